@@ -1,0 +1,175 @@
+/*
+ * sfmg.h -- sum-factorised high-order p-multigrid on one NVIDIA B200 (sm_100a), fp64.
+ *
+ * C ABI of libsfmg.so, the B200-native hot path of Sundar, Stadler & Biros, "Comparison of
+ * multigrid algorithms for high-order continuous finite element discretizations"
+ * (arXiv 1402.5938).  Citations: "P:n" = PAPER.md line n; "R<k>" = DESIGN.md reading k.
+ *
+ * Problem (eq. (1)): -div(mu grad u) = f on the image of [0,1]^3, u = 0 on the
+ * boundary, Galerkin discretisation a(u,v) = int mu grad u . grad v with order-p
+ * tensor LGL nodal bases on a structured hex mesh, isoparametric
+ * geometry and (p+1)^3-point LGL quadrature collocated with the nodes (R1, R2).
+ *
+ * Conventions for every call:
+ *  - All arrays are fp64 (or the stated integer type), contiguous, and CALLER-OWNED.
+ *    Pointers prefixed d_ are device pointers on the current CUDA device, h_ host pointers.
+ *  - Global dof numbering: g = I + Mx (J + My K), I = ex p + a, ...  (lattice of
+ *    Mx = nex p + 1 by My by Mz nodes, x fastest).  Elements e = ex + nex (ey + ney ez),
+ *    local nodes l = a + (p+1)(b + (p+1) c).  Vectors have length N = Mx My Mz including the
+ *    boundary (R17).
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).  Calls are
+ *    asynchronous on that stream unless documented "syncs".  One stream at a time per handle:
+ *    handles own scratch inside the caller's workspace.
+ *  - The library never allocates device memory.  A handle is built inside a caller-allocated
+ *    device workspace whose size the *_query call returns; *_destroy frees host metadata only.
+ *  - Every call returns sfmg_status; argument errors are detected synchronously and leave
+ *    outputs untouched; asynchronous CUDA faults surface at the next synchronising call
+ *    (SFMG_E_CUDA, text in sfmg_last_error()).  No C++ exception crosses the ABI.
+ *  - Dirichlet treatment (R4): bc = 0 applies A_D = M A M + (I - M) with M the interior mask
+ *    (identity rows and columns on the boundary); bc = 1 applies the unprojected A.
+ */
+#ifndef SFMG_H
+#define SFMG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SFMG_OK = 0,
+  SFMG_E_ARG = 1,        /* null pointer, bad enum, vector length != N                       */
+  SFMG_E_ORDER = 2,      /* p < 1 or p > 16                                                 */
+  SFMG_E_MESH = 3,       /* an element count < 1 or a lattice too large for 32-bit indices  */
+  SFMG_E_GEOMETRY = 4,   /* det J <= 0 at some quadrature point (folded element)            */
+  SFMG_E_PCOARSEN = 5,   /* p odd where p/2 is required, or levels not (p, p/2) on one grid */
+  SFMG_E_BREAKDOWN = 6,  /* (p, A p) <= 0 in CG                                             */
+  SFMG_E_WORKSPACE = 7,  /* workspace smaller than the queried size, or misaligned          */
+  SFMG_E_CUDA = 8        /* CUDA error; see sfmg_last_error()                                */
+} sfmg_status;
+
+/* What the paper's problem statement fixes (R3, R5, R6). */
+typedef struct {
+  int32_t nex, ney, nez;   /* elements per direction on [0,1]^3                             */
+  int32_t order;           /* p = 1..16                                                     */
+  int32_t warp;            /* 0 identity; 1: x_i += warp_amp sin(pi x) sin(pi y) sin(pi z)   */
+  double warp_amp;         /*   (reference-cube point mapped per component; boundary fixed)  */
+  int32_t coeff;           /* mu at the physical nodes: 0: c0; 1: exp(c1 S); 2: 10^(c1 S);   */
+  double c0, c1;           /*   3: c0 + c1 sum_i cos^2(2 pi x_i); S = sin2pix sin2piy sin2piz */
+} sfmg_problem;
+
+/* p-multigrid parameters (R7-R11, R13). */
+typedef struct {
+  int32_t nu_pre, nu_post;   /* Chebyshev applications before / after the coarse correction */
+  int32_t cheb_degree;       /* K: steps (= applies) per Chebyshev application               */
+  double eig_lo_frac;        /* interval [lo_frac lambda, hi_frac lambda]; BASELINE 0.1, 1.1  */
+  double eig_hi_frac;
+  int32_t power_iters;       /* lambda_max: power iterations on D^{-1} A_D (R9); 10          */
+  uint64_t power_seed;       /* splitmix64 seed of the power-iteration start vector; 12345   */
+  double coarse_rtol;        /* p = 1 coarse CG: ||r|| <= coarse_rtol ||b||; 1e-10           */
+  int32_t coarse_max_iter;   /* 10000                                                        */
+} sfmg_mg_params;
+
+/* Solve report.  history: caller-owned host buffer of history_cap doubles
+ * receiving ||r_k||_2 for k = 0..iterations (truncated to history_cap), may be NULL. */
+typedef struct {
+  int32_t iterations;        /* outer iterations (MG-solver V-cycles or PCG iterations)      */
+  int32_t converged;         /* 1 iff ||r|| <= rtol ||r0||                                   */
+  double r0_norm, r_norm;
+  int64_t fine_applies;      /* fine-level operator applications, cost model eq. (8)          */
+  int64_t vcycles;           /* V-cycles performed                                            */
+  double* history;
+  int32_t history_cap;
+} sfmg_report;
+
+typedef struct sfmg_level_s* sfmg_level; /* one (mesh, p): G, diag, scratch                    */
+typedef struct sfmg_hier_s* sfmg_hier;   /* levels p, p/2, ..., 1 on one element grid          */
+
+const char* sfmg_version(void);
+/* Text of the last error in this thread ("" if none). */
+const char* sfmg_last_error(void);
+
+/* ---------------------------------------------------------------- level setup */
+/* Sizes of a level: N (dofs incl. boundary), E (elements) and the device workspace bytes. */
+sfmg_status sfmg_level_query(const sfmg_problem* prob, int64_t* n_dofs, int64_t* n_elem,
+                             size_t* ws_bytes);
+/* Build a level inside d_ws (>= ws_bytes, 256-byte aligned): 1-D LGL basis (host), geometric
+ * factors G_q = w_i w_j w_k mu(x_q) detJ_q J_q^{-1} J_q^{-T} at every collocated quadrature
+ * point (device), the diagonal of A_D and its inverse.  Syncs (checks det J > 0:
+ * SFMG_E_GEOMETRY otherwise). */
+sfmg_status sfmg_level_create(const sfmg_problem* prob, void* d_ws, size_t ws_bytes, void* stream,
+                              sfmg_level* out);
+sfmg_status sfmg_level_destroy(sfmg_level lv);
+sfmg_status sfmg_level_info(sfmg_level lv, int64_t* n_dofs, int64_t* n_elem, int32_t* order);
+
+/* Bit-exact exports of the index maps: l2g int32 [E][(p+1)^3];
+ * mask uint8 [N] (1 = boundary); colors uint8 [E] = (ex&1) | (ey&1)<<1 | (ez&1)<<2. */
+sfmg_status sfmg_export_l2g(sfmg_level lv, int32_t* d_l2g, void* stream);
+sfmg_status sfmg_export_mask(sfmg_level lv, uint8_t* d_mask, void* stream);
+sfmg_status sfmg_export_colors(sfmg_level lv, uint8_t* d_colors, void* stream);
+/* Geometric factors as stored, fp64 [E][6][(p+1)^3] with components (00,01,02,11,12,22). */
+sfmg_status sfmg_export_geometry(sfmg_level lv, double* d_G, void* stream);
+
+/* ---------------------------------------------------------------- operator */
+/* d_v = A_D d_u (bc = 0) or A d_u (bc = 1), matrix-free and sum-factorised.  n must be N;
+ * d_u and d_v must not alias. */
+sfmg_status sfmg_apply(sfmg_level lv, int32_t bc, const double* d_u, double* d_v, int64_t n,
+                       void* stream);
+/* diag(A_D) (bc = 0: boundary entries 1) or diag(A) (bc = 1). */
+sfmg_status sfmg_diag(sfmg_level lv, int32_t bc, double* d_diag, int64_t n, void* stream);
+/* lambda_max of D^{-1} A_D by `iters` power iterations with the D-Rayleigh quotient from a
+ * splitmix64(seed) start vector, boundary zeroed (R9).  Syncs. */
+sfmg_status sfmg_lambda_max(sfmg_level lv, int32_t iters, uint64_t seed, double* h_lambda,
+                            void* stream);
+/* One degree-`degree` Chebyshev-accelerated Jacobi application to A_D x = b on the interval
+ * [lam_lo, lam_hi] of D^{-1} A_D (R7, R10): `degree` steps, each one
+ * operator apply.  d_x is the initial guess on input and the smoothed iterate on output. */
+sfmg_status sfmg_cheb(sfmg_level lv, const double* d_b, double* d_x, int64_t n, int32_t degree,
+                      double lam_lo, double lam_hi, void* stream);
+/* Load vector of the manufactured solution u* = sin(pi x) sin(pi y) sin(pi z) (rhs_id 1):
+ * b_g = (1 - bnd_g) sum_{(e,q) -> g} w_q detJ_q f(x_q), f = -div(mu grad u*). */
+sfmg_status sfmg_load_vector(sfmg_level lv, int32_t rhs_id, double* d_f, int64_t n, void* stream);
+
+/* Host-buffer variants (end-to-end path): copy h_u (pinned or pageable) to the level's
+ * device scratch, run the call, copy the result back; syncs.  h_* have length N. */
+sfmg_status sfmg_apply_host(sfmg_level lv, int32_t bc, const double* h_u, double* h_v, int64_t n,
+                            void* stream);
+sfmg_status sfmg_cheb_host(sfmg_level lv, const double* h_b, double* h_x, int64_t n,
+                           int32_t degree, double lam_lo, double lam_hi, void* stream);
+
+/* ---------------------------------------------------------------- p-transfer */
+/* fine.order == 2 coarse.order on the same element grid, else SFMG_E_PCOARSEN.
+ * prolong: d_uf = P0 d_uc with P0 = M_f P M_c, P_gJ = phi^{coarse}_J(xi(g)) (eq. (7)).
+ * restrict: d_rc = P0^T d_rf (R12).  Vectors sized N_coarse / N_fine. */
+sfmg_status sfmg_prolong(sfmg_level coarse, sfmg_level fine, const double* d_uc, double* d_uf,
+                         void* stream);
+sfmg_status sfmg_restrict(sfmg_level coarse, sfmg_level fine, const double* d_rf, double* d_rc,
+                          void* stream);
+
+/* ---------------------------------------------------------------- hierarchy */
+sfmg_status sfmg_hier_query(const sfmg_problem* fine, const sfmg_mg_params* mg, size_t* ws_bytes);
+/* Build levels p, p/2, ..., 1 (geometry rediscretised per level, R20), their diagonals and
+ * lambda_max estimates.  Syncs. */
+sfmg_status sfmg_hier_create(const sfmg_problem* fine, const sfmg_mg_params* mg, void* d_ws,
+                             size_t ws_bytes, void* stream, sfmg_hier* out);
+sfmg_status sfmg_hier_destroy(sfmg_hier h);
+sfmg_status sfmg_hier_info(sfmg_hier h, int32_t* n_levels, int64_t* n_dofs_fine);
+/* Level l (0 = finest) as a level handle owned by the hierarchy (do not destroy). */
+sfmg_status sfmg_hier_level(sfmg_hier h, int32_t l, sfmg_level* out);
+sfmg_status sfmg_hier_lambda(sfmg_hier h, int32_t l, double* h_lambda);
+/* x = V(b) from x = 0: per level nu_pre Chebyshev applications, residual, restriction,
+ * recursion, prolongation + correction, nu_post applications; coarsest (p = 1) by CG
+ * (R11, R13).  No host synchronisation. */
+sfmg_status sfmg_vcycle(sfmg_hier h, const double* d_b, double* d_x, void* stream);
+/* mode 0: MG as solver, x <- x + V(b - A x); mode 1: MG-preconditioned CG (Algorithm 1,
+ * P:973-991).  x0 = 0 (the input content of d_x is ignored), stop at ||r||_2 <= rtol ||r0||_2
+ * (P:1000-1003).  Non-convergence is not an error (converged = 0).  Syncs each iteration. */
+sfmg_status sfmg_solve(sfmg_hier h, int32_t mode, const double* d_b, double* d_x, double rtol,
+                       int32_t max_iter, sfmg_report* report, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SFMG_H */

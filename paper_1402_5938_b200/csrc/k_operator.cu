@@ -1,0 +1,692 @@
+// Operator kernels for sm_100a: geometric factors, the matrix-free sum-factorised stiffness
+// apply (the hot kernel), its diagonal, the Chebyshev update, the load vector, the index-map
+// exports and the single-CTA coarse CG.  fp64 throughout (BASELINE north_star).
+//
+// Element operator, per element e with n = p+1 points/direction:
+//   g0(i,j,k) = sum_m D[i][m] u(m,j,k), g1 = sum_m D[j][m] u(i,m,k), g2 = sum_m D[k][m] u(i,j,m)
+//   w = G_q g                                 (G_q symmetric, 6 unique fp64 per point)
+//   v(a,b,c) = sum_i D[i][a] w0(i,b,c) + sum_j D[j][b] w1(a,j,c) + sum_k D[k][c] w2(a,b,k)
+//   v[l2g(e,.)] += v_e                        (fp64 RED into L2)
+// D[i][m] = ell_m'(xhat_i) lives in __constant__ memory: with p a template parameter every loop
+// is unrolled, every D index is a compile-time constant, and DFMA takes D as a constant-bank
+// operand (no load instruction).
+#include <cstdio>
+
+#include "sfmg_internal.h"
+
+namespace sfmg {
+
+__constant__ double c_D[kMaxOrder][17 * 17];
+__constant__ double c_x[kMaxOrder][17];
+__constant__ double c_w[kMaxOrder][17];
+
+static bool g_uploaded[kMaxOrder + 1];
+
+cudaError_t upload_order_tables(int p, cudaStream_t s) {
+  if (g_uploaded[p]) return cudaSuccess;
+  Basis1D B = make_basis(p);
+  const int n = p + 1;
+  cudaError_t e;
+  e = cudaMemcpyToSymbol(c_D, B.D.data(), sizeof(double) * n * n, sizeof(double) * 17 * 17 * (p - 1));
+  if (e) return e;
+  e = cudaMemcpyToSymbol(c_x, B.x.data(), sizeof(double) * n, sizeof(double) * 17 * (p - 1));
+  if (e) return e;
+  e = cudaMemcpyToSymbol(c_w, B.w.data(), sizeof(double) * n, sizeof(double) * 17 * (p - 1));
+  if (e) return e;
+  g_uploaded[p] = true;
+  (void)s;
+  return cudaSuccess;
+}
+
+// ------------------------------------------------------------------------------------------
+// small device helpers
+
+__device__ __forceinline__ void elem_coords(const MeshDev& m, long long e, int& ex, int& ey, int& ez) {
+  ex = (int)(e % m.nex);
+  long long t = e / m.nex;
+  ey = (int)(t % m.ney);
+  ez = (int)(t / m.ney);
+}
+
+__device__ __forceinline__ bool lattice_boundary(const MeshDev& m, long long g) {
+  unsigned int gi = (unsigned int)g;
+  unsigned int I = gi % (unsigned)m.Mx;
+  unsigned int r = gi / (unsigned)m.Mx;
+  unsigned int J = r % (unsigned)m.My;
+  unsigned int K = r / (unsigned)m.My;
+  return I == 0 || I == (unsigned)m.Mx - 1 || J == 0 || J == (unsigned)m.My - 1 || K == 0 ||
+         K == (unsigned)m.Mz - 1;
+}
+
+// mu at a physical point (R3, R6)
+__device__ __forceinline__ double coeff_mu(const MeshDev& m, double x, double y, double z) {
+  switch (m.coeff) {
+    case 0: return m.c0;
+    case 1: return exp(m.c1 * sinpi(2.0 * x) * sinpi(2.0 * y) * sinpi(2.0 * z));
+    case 2: return exp10(m.c1 * sinpi(2.0 * x) * sinpi(2.0 * y) * sinpi(2.0 * z));
+    case 3: {
+      double a = cospi(2.0 * x), b = cospi(2.0 * y), c = cospi(2.0 * z);
+      return m.c0 + m.c1 * (a * a + b * b + c * c);
+    }
+  }
+  return 0.0;
+}
+
+__device__ __forceinline__ void coeff_grad(const MeshDev& m, double x, double y, double z, double mu,
+                                           double g[3]) {
+  const double tp = 6.283185307179586476925;
+  double sx = sinpi(2.0 * x), sy = sinpi(2.0 * y), sz = sinpi(2.0 * z);
+  double cx = cospi(2.0 * x), cy = cospi(2.0 * y), cz = cospi(2.0 * z);
+  double dS0 = tp * cx * sy * sz, dS1 = tp * sx * cy * sz, dS2 = tp * sx * sy * cz;
+  double f = 0.0;
+  switch (m.coeff) {
+    case 0: g[0] = g[1] = g[2] = 0.0; return;
+    case 1: f = m.c1 * mu; break;
+    case 2: f = 2.302585092994045684018 * m.c1 * mu; break;
+    case 3:
+      g[0] = -tp * m.c1 * sinpi(4.0 * x);
+      g[1] = -tp * m.c1 * sinpi(4.0 * y);
+      g[2] = -tp * m.c1 * sinpi(4.0 * z);
+      return;
+  }
+  g[0] = f * dS0; g[1] = f * dS1; g[2] = f * dS2;
+}
+
+// Physical position of local node (a,b,c) of element (ex,ey,ez): reference-cube lattice point
+// then the warp x_i += amp sin(pi X) sin(pi Y) sin(pi Z) (R5).
+template <int P>
+__device__ __forceinline__ void node_pos(const MeshDev& m, const double* xs, int ex, int ey, int ez,
+                                         int a, int b, int c, double X[3]) {
+  double Xr = (ex + 0.5 * (xs[a] + 1.0)) / m.nex;
+  double Yr = (ey + 0.5 * (xs[b] + 1.0)) / m.ney;
+  double Zr = (ez + 0.5 * (xs[c] + 1.0)) / m.nez;
+  double s = 0.0;
+  if (m.warp == 1) s = m.amp * sinpi(Xr) * sinpi(Yr) * sinpi(Zr);
+  X[0] = Xr + s; X[1] = Yr + s; X[2] = Zr + s;
+}
+
+// Isoparametric Jacobian at collocated point (i,j,k): J[al][be] = d x_al / d xi_be
+// = sum_m D[.][m] x_al along the be-line through the point (R2).
+template <int P>
+__device__ __forceinline__ void jacobian(const MeshDev& m, const double* sD, const double* xs, int ex,
+                                         int ey, int ez, int i, int j, int k, double J[3][3]) {
+  constexpr int N = P + 1;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) J[a][0] = J[a][1] = J[a][2] = 0.0;
+  for (int mm = 0; mm < N; ++mm) {
+    double X[3];
+    node_pos<P>(m, xs, ex, ey, ez, mm, j, k, X);
+    double d = sD[i * N + mm];
+    J[0][0] += d * X[0]; J[1][0] += d * X[1]; J[2][0] += d * X[2];
+    node_pos<P>(m, xs, ex, ey, ez, i, mm, k, X);
+    d = sD[j * N + mm];
+    J[0][1] += d * X[0]; J[1][1] += d * X[1]; J[2][1] += d * X[2];
+    node_pos<P>(m, xs, ex, ey, ez, i, j, mm, X);
+    d = sD[k * N + mm];
+    J[0][2] += d * X[0]; J[1][2] += d * X[1]; J[2][2] += d * X[2];
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// K1 geometric factors: one thread per (element, point), G [E][6][n^3].
+
+template <int P>
+__global__ void __launch_bounds__(256) k_geometry(MeshDev m, double* __restrict__ G, int* bad) {
+  constexpr int N = P + 1, N2 = N * N, N3 = N2 * N;
+  __shared__ double sD[N * N], sx[N], sw[N];
+  for (int t = threadIdx.x; t < N * N; t += blockDim.x) sD[t] = c_D[P - 1][t];
+  for (int t = threadIdx.x; t < N; t += blockDim.x) { sx[t] = c_x[P - 1][t]; sw[t] = c_w[P - 1][t]; }
+  __syncthreads();
+  const long long total = m.E * N3;
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    long long e = idx / N3;
+    int q = (int)(idx - e * N3);
+    int i = q % N, j = (q / N) % N, k = q / N2;
+    int ex, ey, ez;
+    elem_coords(m, e, ex, ey, ez);
+    double J[3][3];
+    jacobian<P>(m, sD, sx, ex, ey, ez, i, j, k, J);
+    double det = J[0][0] * (J[1][1] * J[2][2] - J[1][2] * J[2][1]) -
+                 J[0][1] * (J[1][0] * J[2][2] - J[1][2] * J[2][0]) +
+                 J[0][2] * (J[1][0] * J[2][1] - J[1][1] * J[2][0]);
+    if (!(det > 0.0)) atomicAdd(bad, 1);
+    double id = 1.0 / det;
+    double Ji[3][3];
+    Ji[0][0] = (J[1][1] * J[2][2] - J[1][2] * J[2][1]) * id;
+    Ji[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) * id;
+    Ji[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) * id;
+    Ji[1][0] = (J[1][2] * J[2][0] - J[1][0] * J[2][2]) * id;
+    Ji[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) * id;
+    Ji[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * id;
+    Ji[2][0] = (J[1][0] * J[2][1] - J[1][1] * J[2][0]) * id;
+    Ji[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) * id;
+    Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * id;
+    double X[3];
+    node_pos<P>(m, sx, ex, ey, ez, i, j, k, X);
+    double s = sw[i] * sw[j] * sw[k] * coeff_mu(m, X[0], X[1], X[2]) * det;
+    double* Ge = G + e * 6 * N3 + q;
+    const int comp[6][2] = {{0, 0}, {0, 1}, {0, 2}, {1, 1}, {1, 2}, {2, 2}};
+#pragma unroll
+    for (int c = 0; c < 6; ++c) {
+      int a = comp[c][0], b = comp[c][1];
+      Ge[c * N3] = s * (Ji[a][0] * Ji[b][0] + Ji[a][1] * Ji[b][1] + Ji[a][2] * Ji[b][2]);
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// K2 apply.  Block = EPB elements x (n x n) threads.  Thread t = (t0, t1) of an element owns
+// one 1-D line per phase:
+//   gather   : column (i=t0, j=t1) over k       -> registers ru[] and smem su
+//   P1       : x-line (j=t0, k=t1): g0 = D u     -> s0
+//   P2       : y-line (i=t0, k=t1): g1 = D u     -> s1
+//   P3       : z-line (i=t0, j=t1): g2 = D ru (registers), w = G g (G streamed from HBM,
+//              coalesced over the (i,j) slab), w0 -> s0, w1 -> s1, vz = D^T w2 (registers)
+//   P4       : x-line: v0 = D^T w0 -> su
+//   P5       : y-line: su += D^T w1
+//   P6       : z-line: v = su + vz, RED.ADD into v[g] (interior rows only for bc 0)
+// Each line pass reads n values and does n^2 FMAs, so the shared-memory traffic is ~14 n^3
+// doubles per element against 6 n^4 FMAs.
+
+template <int P>
+struct ApplyCfg {
+  static constexpr int N = P + 1, N2 = N * N, N3 = N2 * N;
+  static constexpr int EPB = (256 / N2) > 0 ? (256 / N2) : 1;
+  static constexpr int THREADS = EPB * N2;
+  static constexpr size_t SMEM = (size_t)EPB * 3 * N3 * sizeof(double);
+};
+
+template <int P, bool DIR>
+__global__ void __launch_bounds__(ApplyCfg<P>::THREADS)
+    k_apply(MeshDev m, const double* __restrict__ G, const double* __restrict__ u, double* __restrict__ v) {
+  using C = ApplyCfg<P>;
+  constexpr int N = C::N, N2 = C::N2, N3 = C::N3;
+  extern __shared__ double smem[];
+  const int le = threadIdx.x / N2;
+  const int t = threadIdx.x - le * N2;
+  const int t0 = t % N, t1 = t / N;
+  const long long e = (long long)blockIdx.x * C::EPB + le;
+  const bool act = e < m.E;
+  double* su = smem + le * 3 * N3;
+  double* s0 = su + N3;
+  double* s1 = s0 + N3;
+
+  int ex = 0, ey = 0, ez = 0;
+  if (act) elem_coords(m, e, ex, ey, ez);
+  const long long sxy = (long long)m.Mx * m.My;
+  const long long gcol = (long long)(ex * P + t0) + (long long)m.Mx * (ey * P + t1) + sxy * (long long)(ez * P);
+  bool bxy = false;
+  if (DIR) {
+    const int I = ex * P + t0, J = ey * P + t1;
+    bxy = (I == 0) || (I == m.Mx - 1) || (J == 0) || (J == m.My - 1);
+  }
+
+  double ru[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    double val = 0.0;
+    if (act) {
+      bool bnd = false;
+      if (DIR) { const int K = ez * P + k; bnd = bxy || K == 0 || K == m.Mz - 1; }
+      if (!bnd) val = __ldg(u + gcol + sxy * k);
+    }
+    ru[k] = val;
+    su[t0 + N * t1 + N2 * k] = val;
+  }
+  __syncthreads();
+
+  {  // P1: x-derivative on line (j=t0, k=t1)
+    double L[N];
+#pragma unroll
+    for (int mm = 0; mm < N; ++mm) L[mm] = su[mm + N * t0 + N2 * t1];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      double s = 0.0;
+#pragma unroll
+      for (int mm = 0; mm < N; ++mm) s = fma(c_D[P - 1][i * N + mm], L[mm], s);
+      s0[i + N * t0 + N2 * t1] = s;
+    }
+  }
+  {  // P2: y-derivative on line (i=t0, k=t1)
+    double L[N];
+#pragma unroll
+    for (int mm = 0; mm < N; ++mm) L[mm] = su[t0 + N * mm + N2 * t1];
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      double s = 0.0;
+#pragma unroll
+      for (int mm = 0; mm < N; ++mm) s = fma(c_D[P - 1][j * N + mm], L[mm], s);
+      s1[t0 + N * j + N2 * t1] = s;
+    }
+  }
+  __syncthreads();
+
+  double vz[N];
+  {  // P3: z-derivative in registers, pointwise metric product, z-transpose in registers
+    const double* Ge = G + (act ? e : 0) * 6 * N3 + t0 + N * t1;
+    double w2[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      double g2 = 0.0;
+#pragma unroll
+      for (int mm = 0; mm < N; ++mm) g2 = fma(c_D[P - 1][k * N + mm], ru[mm], g2);
+      const int idx = t0 + N * t1 + N2 * k;
+      const double g0 = s0[idx], g1 = s1[idx];
+      double G00 = 0, G01 = 0, G02 = 0, G11 = 0, G12 = 0, G22 = 0;
+      if (act) {
+        G00 = __ldcs(Ge + 0 * N3 + N2 * k);
+        G01 = __ldcs(Ge + 1 * N3 + N2 * k);
+        G02 = __ldcs(Ge + 2 * N3 + N2 * k);
+        G11 = __ldcs(Ge + 3 * N3 + N2 * k);
+        G12 = __ldcs(Ge + 4 * N3 + N2 * k);
+        G22 = __ldcs(Ge + 5 * N3 + N2 * k);
+      }
+      s0[idx] = G00 * g0 + G01 * g1 + G02 * g2;
+      s1[idx] = G01 * g0 + G11 * g1 + G12 * g2;
+      w2[k] = G02 * g0 + G12 * g1 + G22 * g2;
+    }
+#pragma unroll
+    for (int c = 0; c < N; ++c) {
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < N; ++k) s = fma(c_D[P - 1][k * N + c], w2[k], s);
+      vz[c] = s;
+    }
+  }
+  __syncthreads();
+
+  {  // P4: v0 = D^T w0 on x-line (j=t0, k=t1) -> su
+    double L[N];
+#pragma unroll
+    for (int mm = 0; mm < N; ++mm) L[mm] = s0[mm + N * t0 + N2 * t1];
+#pragma unroll
+    for (int a = 0; a < N; ++a) {
+      double s = 0.0;
+#pragma unroll
+      for (int mm = 0; mm < N; ++mm) s = fma(c_D[P - 1][mm * N + a], L[mm], s);
+      su[a + N * t0 + N2 * t1] = s;
+    }
+  }
+  __syncthreads();
+  {  // P5: su += D^T w1 on y-line (i=t0, k=t1)
+    double L[N];
+#pragma unroll
+    for (int mm = 0; mm < N; ++mm) L[mm] = s1[t0 + N * mm + N2 * t1];
+#pragma unroll
+    for (int b = 0; b < N; ++b) {
+      double s = 0.0;
+#pragma unroll
+      for (int mm = 0; mm < N; ++mm) s = fma(c_D[P - 1][mm * N + b], L[mm], s);
+      su[t0 + N * b + N2 * t1] += s;
+    }
+  }
+  __syncthreads();
+  if (act) {  // P6: z-line (i=t0, j=t1): assemble and scatter
+#pragma unroll
+    for (int c = 0; c < N; ++c) {
+      bool bnd = false;
+      if (DIR) { const int K = ez * P + c; bnd = bxy || K == 0 || K == m.Mz - 1; }
+      if (!bnd) atomicAdd(v + gcol + sxy * c, su[t0 + N * t1 + N2 * c] + vz[c]);
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// K3 diagonal: for node (a,b,c) of element e
+//   sum_i D[i][a]^2 G00(i,b,c) + sum_j D[j][b]^2 G11(a,j,c) + sum_k D[k][c]^2 G22(a,b,k)
+//   + 2 D[a][a] D[b][b] G01(a,b,c) + 2 D[a][a] D[c][c] G02(a,b,c) + 2 D[b][b] D[c][c] G12(a,b,c)
+
+template <int P>
+__global__ void __launch_bounds__(256) k_diag(MeshDev m, int bc, const double* __restrict__ G, double* d) {
+  constexpr int N = P + 1, N2 = N * N, N3 = N2 * N;
+  __shared__ double sD[N * N];
+  for (int t = threadIdx.x; t < N * N; t += blockDim.x) sD[t] = c_D[P - 1][t];
+  __syncthreads();
+  const long long total = m.E * N3;
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    long long e = idx / N3;
+    int l = (int)(idx - e * N3);
+    int a = l % N, b = (l / N) % N, c = l / N2;
+    int ex, ey, ez;
+    elem_coords(m, e, ex, ey, ez);
+    long long g = (long long)(ex * P + a) + (long long)m.Mx * ((long long)(ey * P + b) + (long long)m.My * (ez * P + c));
+    if (bc == 0 && lattice_boundary(m, g)) continue;
+    const double* Ge = G + e * 6 * N3;
+    double s = 0.0;
+    for (int i = 0; i < N; ++i) s += sD[i * N + a] * sD[i * N + a] * Ge[0 * N3 + i + N * b + N2 * c];
+    for (int j = 0; j < N; ++j) s += sD[j * N + b] * sD[j * N + b] * Ge[3 * N3 + a + N * j + N2 * c];
+    for (int k = 0; k < N; ++k) s += sD[k * N + c] * sD[k * N + c] * Ge[5 * N3 + a + N * b + N2 * k];
+    const double da = sD[a * N + a], db = sD[b * N + b], dc = sD[c * N + c];
+    s += 2.0 * da * db * Ge[1 * N3 + l] + 2.0 * da * dc * Ge[2 * N3 + l] + 2.0 * db * dc * Ge[4 * N3 + l];
+    atomicAdd(d + g, s);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// Load vector of u* = sin(pi x) sin(pi y) sin(pi z).
+
+template <int P>
+__global__ void __launch_bounds__(256) k_load(MeshDev m, double* f) {
+  constexpr int N = P + 1, N2 = N * N, N3 = N2 * N;
+  __shared__ double sD[N * N], sx[N], sw[N];
+  for (int t = threadIdx.x; t < N * N; t += blockDim.x) sD[t] = c_D[P - 1][t];
+  for (int t = threadIdx.x; t < N; t += blockDim.x) { sx[t] = c_x[P - 1][t]; sw[t] = c_w[P - 1][t]; }
+  __syncthreads();
+  const double pi = 3.14159265358979323846;
+  const long long total = m.E * N3;
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    long long e = idx / N3;
+    int q = (int)(idx - e * N3);
+    int i = q % N, j = (q / N) % N, k = q / N2;
+    int ex, ey, ez;
+    elem_coords(m, e, ex, ey, ez);
+    long long g = (long long)(ex * P + i) + (long long)m.Mx * ((long long)(ey * P + j) + (long long)m.My * (ez * P + k));
+    if (lattice_boundary(m, g)) continue;
+    double J[3][3];
+    jacobian<P>(m, sD, sx, ex, ey, ez, i, j, k, J);
+    double det = J[0][0] * (J[1][1] * J[2][2] - J[1][2] * J[2][1]) -
+                 J[0][1] * (J[1][0] * J[2][2] - J[1][2] * J[2][0]) +
+                 J[0][2] * (J[1][0] * J[2][1] - J[1][1] * J[2][0]);
+    double X[3];
+    node_pos<P>(m, sx, ex, ey, ez, i, j, k, X);
+    double s0 = sinpi(X[0]), s1 = sinpi(X[1]), s2 = sinpi(X[2]);
+    double c0 = cospi(X[0]), c1 = cospi(X[1]), c2 = cospi(X[2]);
+    double us = s0 * s1 * s2;
+    double gu[3] = {pi * c0 * s1 * s2, pi * s0 * c1 * s2, pi * s0 * s1 * c2};
+    double mu = coeff_mu(m, X[0], X[1], X[2]);
+    double gm[3];
+    coeff_grad(m, X[0], X[1], X[2], mu, gm);
+    double fx = 3.0 * pi * pi * mu * us - (gm[0] * gu[0] + gm[1] * gu[1] + gm[2] * gu[2]);
+    atomicAdd(f + g, sw[i] * sw[j] * sw[k] * det * fx);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// vector kernels that need the lattice
+
+__global__ void k_init(MeshDev m, int bc, const double* __restrict__ u, double bval, double* __restrict__ v) {
+  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < m.N; g += (long long)gridDim.x * blockDim.x) {
+    double val = 0.0;
+    if (bc == 0 && lattice_boundary(m, g)) val = u ? u[g] : bval;
+    v[g] = val;
+  }
+}
+
+__global__ void k_cheb_update(MeshDev m, const double* cur, const double* prev, double* out,
+                              const double* __restrict__ b, double* y, const double* __restrict__ dinv,
+                              double c1, double c2) {
+  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < m.N; g += (long long)gridDim.x * blockDim.x) {
+    const double xc = cur[g];
+    const double xp = (c1 != 0.0) ? prev[g] : 0.0;
+    const double xn = xc + c1 * (xc - xp) + c2 * dinv[g] * (b[g] - y[g]);
+    out[g] = xn;
+    y[g] = lattice_boundary(m, g) ? xn : 0.0;
+  }
+}
+
+__global__ void k_export_maps(MeshDev m, int32_t* l2g, uint8_t* mask, uint8_t* col) {
+  const int P = m.p, N = P + 1;
+  const long long N3 = (long long)N * N * N;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (l2g)
+    for (long long idx = t0; idx < m.E * N3; idx += stride) {
+      long long e = idx / N3;
+      int l = (int)(idx - e * N3);
+      int a = l % N, b = (l / N) % N, c = l / (N * N);
+      int ex, ey, ez;
+      elem_coords(m, e, ex, ey, ez);
+      l2g[idx] = (int32_t)((long long)(ex * P + a) + (long long)m.Mx * ((long long)(ey * P + b) + (long long)m.My * (ez * P + c)));
+    }
+  if (mask)
+    for (long long g = t0; g < m.N; g += stride) mask[g] = lattice_boundary(m, g) ? 1 : 0;
+  if (col)
+    for (long long e = t0; e < m.E; e += stride) {
+      int ex, ey, ez;
+      elem_coords(m, e, ex, ey, ez);
+      col[e] = (uint8_t)((ex & 1) | ((ey & 1) << 1) | ((ez & 1) << 2));
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// K8 coarse CG (R13): one CTA runs the whole unpreconditioned CG loop on the p = 1 level, so a
+// V-cycle needs no host synchronisation.  Vectors live in global memory (L2-resident at these
+// sizes) and are re-read with ld.global.cg, bypassing the incoherent L1.
+
+__device__ double block_sum(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+  __syncthreads();
+  if (ln == 0) red[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  const int nw = (blockDim.x + 31) >> 5;
+  for (int i = 0; i < nw; ++i) s += red[i];
+  return s;
+}
+
+template <int P>
+__device__ void cta_apply(const MeshDev& m, const double* __restrict__ G, const double* x, double* y) {
+  constexpr int N = P + 1, N2 = N * N, N3 = N2 * N;
+  for (long long g = threadIdx.x; g < m.N; g += blockDim.x) y[g] = lattice_boundary(m, g) ? __ldcg(x + g) : 0.0;
+  __syncthreads();
+  for (long long e = threadIdx.x; e < m.E; e += blockDim.x) {
+    int ex, ey, ez;
+    elem_coords(m, e, ex, ey, ez);
+    double ue[N3], ve[N3];
+    long long gl[N3];
+#pragma unroll
+    for (int c = 0; c < N; ++c)
+#pragma unroll
+      for (int b = 0; b < N; ++b)
+#pragma unroll
+        for (int a = 0; a < N; ++a) {
+          const int l = a + N * (b + N * c);
+          long long g = (long long)(ex * P + a) + (long long)m.Mx * ((long long)(ey * P + b) + (long long)m.My * (ez * P + c));
+          const bool bnd = lattice_boundary(m, g);
+          gl[l] = bnd ? -1 : g;
+          ue[l] = bnd ? 0.0 : __ldcg(x + g);
+          ve[l] = 0.0;
+        }
+    const double* Ge = G + e * 6 * N3;
+#pragma unroll
+    for (int k = 0; k < N; ++k)
+#pragma unroll
+      for (int j = 0; j < N; ++j)
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          const int q = i + N * (j + N * k);
+          double g0 = 0, g1 = 0, g2 = 0;
+#pragma unroll
+          for (int mm = 0; mm < N; ++mm) {
+            g0 = fma(c_D[P - 1][i * N + mm], ue[mm + N * (j + N * k)], g0);
+            g1 = fma(c_D[P - 1][j * N + mm], ue[i + N * (mm + N * k)], g1);
+            g2 = fma(c_D[P - 1][k * N + mm], ue[i + N * (j + N * mm)], g2);
+          }
+          const double G00 = Ge[q], G01 = Ge[N3 + q], G02 = Ge[2 * N3 + q];
+          const double G11 = Ge[3 * N3 + q], G12 = Ge[4 * N3 + q], G22 = Ge[5 * N3 + q];
+          const double w0 = G00 * g0 + G01 * g1 + G02 * g2;
+          const double w1 = G01 * g0 + G11 * g1 + G12 * g2;
+          const double w2 = G02 * g0 + G12 * g1 + G22 * g2;
+#pragma unroll
+          for (int mm = 0; mm < N; ++mm) {
+            ve[mm + N * (j + N * k)] = fma(c_D[P - 1][i * N + mm], w0, ve[mm + N * (j + N * k)]);
+            ve[i + N * (mm + N * k)] = fma(c_D[P - 1][j * N + mm], w1, ve[i + N * (mm + N * k)]);
+            ve[i + N * (j + N * mm)] = fma(c_D[P - 1][k * N + mm], w2, ve[i + N * (j + N * mm)]);
+          }
+        }
+#pragma unroll
+    for (int l = 0; l < N3; ++l)
+      if (gl[l] >= 0) atomicAdd(y + gl[l], ve[l]);
+  }
+  __threadfence_block();
+  __syncthreads();
+}
+
+template <int P>
+__global__ void __launch_bounds__(1024) k_coarse_cg(MeshDev m, const double* __restrict__ G, const double* b,
+                                                    double* x, double* r, double* p, double* q, double* scal,
+                                                    double rtol, int maxit) {
+  __shared__ double red[32];
+  const long long n = m.N;
+  double rr = 0.0;
+  for (long long g = threadIdx.x; g < n; g += blockDim.x) {
+    const double bg = b[g];
+    x[g] = 0.0; r[g] = bg; p[g] = bg;
+    rr += bg * bg;
+  }
+  rr = block_sum(rr, red);
+  const double bn = sqrt(rr);
+  int it = 0, status = 0;
+  if (bn > 0.0) {
+    for (; it < maxit; ++it) {
+      if (sqrt(rr) <= rtol * bn) break;
+      __syncthreads();
+      cta_apply<P>(m, G, p, q);
+      double pq = 0.0;
+      for (long long g = threadIdx.x; g < n; g += blockDim.x) pq += __ldcg(p + g) * __ldcg(q + g);
+      pq = block_sum(pq, red);
+      if (!(pq > 0.0)) { status = 6; break; }
+      const double alpha = rr / pq;
+      double rn = 0.0;
+      for (long long g = threadIdx.x; g < n; g += blockDim.x) {
+        x[g] = __ldcg(x + g) + alpha * __ldcg(p + g);
+        const double rg = __ldcg(r + g) - alpha * __ldcg(q + g);
+        r[g] = rg;
+        rn += rg * rg;
+      }
+      rn = block_sum(rn, red);
+      const double beta = rn / rr;
+      for (long long g = threadIdx.x; g < n; g += blockDim.x) p[g] = __ldcg(r + g) + beta * __ldcg(p + g);
+      rr = rn;
+      __threadfence_block();
+      __syncthreads();
+    }
+  }
+  if (threadIdx.x == 0) { scal[8] = (double)it; scal[9] = sqrt(rr); scal[10] = (double)status; }
+}
+
+// ------------------------------------------------------------------------------------------
+// launchers
+
+static int grid_for(long long work, int threads) {
+  long long b = (work + threads - 1) / threads;
+  if (b > 148LL * 16) b = 148LL * 16;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+#define SFMG_DISPATCH_P(p, F, ...)  \
+  switch (p) {                      \
+    case 1: F<1>(__VA_ARGS__); break;   \
+    case 2: F<2>(__VA_ARGS__); break;   \
+    case 3: F<3>(__VA_ARGS__); break;   \
+    case 4: F<4>(__VA_ARGS__); break;   \
+    case 5: F<5>(__VA_ARGS__); break;   \
+    case 6: F<6>(__VA_ARGS__); break;   \
+    case 7: F<7>(__VA_ARGS__); break;   \
+    case 8: F<8>(__VA_ARGS__); break;   \
+    case 9: F<9>(__VA_ARGS__); break;   \
+    case 10: F<10>(__VA_ARGS__); break; \
+    case 11: F<11>(__VA_ARGS__); break; \
+    case 12: F<12>(__VA_ARGS__); break; \
+    case 13: F<13>(__VA_ARGS__); break; \
+    case 14: F<14>(__VA_ARGS__); break; \
+    case 15: F<15>(__VA_ARGS__); break; \
+    case 16: F<16>(__VA_ARGS__); break; \
+    default: return cudaErrorInvalidValue; \
+  }
+
+template <int P>
+static void geometry_p(const MeshDev& m, double* G, int* bad, cudaStream_t s) {
+  constexpr int N3 = (P + 1) * (P + 1) * (P + 1);
+  k_geometry<P><<<grid_for(m.E * N3, 256), 256, 0, s>>>(m, G, bad);
+}
+cudaError_t launch_geometry(const MeshDev& m, double* G, int* bad, cudaStream_t s) {
+  SFMG_DISPATCH_P(m.p, geometry_p, m, G, bad, s);
+  return cudaGetLastError();
+}
+
+template <int P, bool DIR>
+static cudaError_t apply_pd(const MeshDev& m, const double* G, const double* u, double* v, cudaStream_t s) {
+  using C = ApplyCfg<P>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_apply<P, DIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    if (e) return e;
+    attr = true;
+  }
+  const long long blocks = (m.E + C::EPB - 1) / C::EPB;
+  k_apply<P, DIR><<<(unsigned)blocks, C::THREADS, C::SMEM, s>>>(m, G, u, v);
+  return cudaSuccess;
+}
+template <int P>
+static void apply_p(const MeshDev& m, int bc, const double* G, const double* u, double* v, cudaStream_t s,
+                    cudaError_t* err) {
+  *err = (bc == 0) ? apply_pd<P, true>(m, G, u, v, s) : apply_pd<P, false>(m, G, u, v, s);
+}
+cudaError_t launch_apply(const MeshDev& m, int bc, const double* G, const double* u, double* v, cudaStream_t s) {
+  cudaError_t err = cudaSuccess;
+  SFMG_DISPATCH_P(m.p, apply_p, m, bc, G, u, v, s, &err);
+  if (err) return err;
+  return cudaGetLastError();
+}
+
+template <int P>
+static void diag_p(const MeshDev& m, int bc, const double* G, double* d, cudaStream_t s) {
+  constexpr int N3 = (P + 1) * (P + 1) * (P + 1);
+  k_diag<P><<<grid_for(m.E * N3, 256), 256, 0, s>>>(m, bc, G, d);
+}
+cudaError_t launch_diag(const MeshDev& m, int bc, const double* G, double* d, cudaStream_t s) {
+  cudaError_t e = launch_init(m, bc, nullptr, 1.0, d, s);
+  if (e) return e;
+  SFMG_DISPATCH_P(m.p, diag_p, m, bc, G, d, s);
+  return cudaGetLastError();
+}
+
+template <int P>
+static void load_p(const MeshDev& m, double* f, cudaStream_t s) {
+  constexpr int N3 = (P + 1) * (P + 1) * (P + 1);
+  k_load<P><<<grid_for(m.E * N3, 256), 256, 0, s>>>(m, f);
+}
+cudaError_t launch_load(const MeshDev& m, int rhs_id, double* f, cudaStream_t s) {
+  if (rhs_id != 1) return cudaErrorInvalidValue;
+  cudaError_t e = launch_init(m, 1, nullptr, 0.0, f, s);
+  if (e) return e;
+  SFMG_DISPATCH_P(m.p, load_p, m, f, s);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_init(const MeshDev& m, int bc, const double* u, double bval, double* v, cudaStream_t s) {
+  k_init<<<grid_for(m.N, 256), 256, 0, s>>>(m, bc, u, bval, v);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cheb_update(const MeshDev& m, const double* cur, const double* prev, double* out,
+                               const double* b, double* y, const double* dinv, double c1, double c2,
+                               cudaStream_t s) {
+  k_cheb_update<<<grid_for(m.N, 256), 256, 0, s>>>(m, cur, prev, out, b, y, dinv, c1, c2);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_export_maps(const MeshDev& m, int32_t* l2g, uint8_t* mask, uint8_t* col, cudaStream_t s) {
+  long long work = m.E * (long long)(m.p + 1) * (m.p + 1) * (m.p + 1);
+  k_export_maps<<<grid_for(work, 256), 256, 0, s>>>(m, l2g, mask, col);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_coarse_cg(const MeshDev& m, const double* G, const double* b, double* x, double* r,
+                             double* p, double* q, double* scal, double rtol, int maxit, cudaStream_t s) {
+  if (m.p == 1)
+    k_coarse_cg<1><<<1, 1024, 0, s>>>(m, G, b, x, r, p, q, scal, rtol, maxit);
+  else if (m.p == 2)
+    k_coarse_cg<2><<<1, 1024, 0, s>>>(m, G, b, x, r, p, q, scal, rtol, maxit);
+  else
+    return cudaErrorInvalidValue;
+  return cudaGetLastError();
+}
+
+}  // namespace sfmg

@@ -1,0 +1,209 @@
+// p-multigrid transfer kernels for sm_100a (eq. (7)).
+//
+// Prolongation p/2 -> p on one element grid: P_gJ = phi^{p/2}_J(xi(g)); per element this is the
+// tensor contraction u_f(i,j,k) = sum_{abc} I[i][a] I[j][b] I[k][c] u_c(a,b,c) with the 1-D
+// interpolation matrix I[i][a] = ell^{p/2}_a(xhat^p_i), evaluated sum-factorised (x, y, z passes
+// through shared memory).  P0 = M_f P M_c: coarse boundary values are read as 0 and fine boundary
+// rows are not written (add) or written as 0 (overwrite).  Every fine node is written once, by its
+// canonical (lowest-index) element, so no atomics are needed.
+// Restriction is the exact transpose: each element contracts the fine values it owns with I^T
+// and adds the coarse result into r_c (fp64 RED), coarse boundary rows excluded (R12).
+#include "sfmg_internal.h"
+
+namespace sfmg {
+
+__constant__ double c_I[8][17 * 9];   // c_I[pc-1][i*(pc+1)+a], fine order 2 pc
+static bool g_interp_uploaded[9];
+
+cudaError_t upload_interp_tables(int pc, cudaStream_t s) {
+  (void)s;
+  if (pc < 1 || pc > 8) return cudaErrorInvalidValue;
+  if (g_interp_uploaded[pc]) return cudaSuccess;
+  std::vector<double> I = make_interp(pc, 2 * pc);
+  cudaError_t e = cudaMemcpyToSymbol(c_I, I.data(), sizeof(double) * I.size(), sizeof(double) * 17 * 9 * (pc - 1));
+  if (e) return e;
+  g_interp_uploaded[pc] = true;
+  return cudaSuccess;
+}
+
+__device__ __forceinline__ void ecoords(const MeshDev& m, long long e, int& ex, int& ey, int& ez) {
+  ex = (int)(e % m.nex);
+  long long t = e / m.nex;
+  ey = (int)(t % m.ney);
+  ez = (int)(t / m.ney);
+}
+
+template <int PC>
+struct XferCfg {
+  static constexpr int PF = 2 * PC, NC = PC + 1, NF = PF + 1;
+  static constexpr int NC3 = NC * NC * NC, NF3 = NF * NF * NF;
+  static constexpr int T1 = NF * NC * NC, T2 = NF * NF * NC;      // prolong intermediates
+  static constexpr int R1 = NC * NF * NF, R2 = NC * NC * NF;      // restrict intermediates
+  static constexpr size_t SMEM_P = sizeof(double) * (NC3 + T1 + T2);
+  static constexpr size_t SMEM_R = sizeof(double) * (NF3 + R1 + R2);
+};
+
+template <int PC>
+__global__ void __launch_bounds__(256) k_prolong(MeshDev mc, MeshDev mf, const double* __restrict__ uc,
+                                                 double* __restrict__ uf, int add) {
+  using C = XferCfg<PC>;
+  constexpr int NC = C::NC, NF = C::NF, PF = C::PF;
+  extern __shared__ double sm[];
+  double* sc = sm;             // [c][b][a]
+  double* t1 = sc + C::NC3;    // [c][b][i]
+  double* t2 = t1 + C::T1;     // [c][j][i]
+  const double* I = c_I[PC - 1];
+  const long long e = blockIdx.x;
+  int ex, ey, ez;
+  ecoords(mf, e, ex, ey, ez);
+  for (int l = threadIdx.x; l < C::NC3; l += blockDim.x) {
+    const int a = l % NC, b = (l / NC) % NC, c = l / (NC * NC);
+    const int I0 = ex * PC + a, J0 = ey * PC + b, K0 = ez * PC + c;
+    const bool bnd = I0 == 0 || I0 == mc.Mx - 1 || J0 == 0 || J0 == mc.My - 1 || K0 == 0 || K0 == mc.Mz - 1;
+    sc[l] = bnd ? 0.0 : uc[I0 + (long long)mc.Mx * (J0 + (long long)mc.My * K0)];
+  }
+  __syncthreads();
+  for (int l = threadIdx.x; l < C::T1; l += blockDim.x) {
+    const int i = l % NF, r = l / NF;     // r = b + NC c
+    double s = 0.0;
+#pragma unroll
+    for (int a = 0; a < NC; ++a) s += I[i * NC + a] * sc[a + NC * r];
+    t1[l] = s;
+  }
+  __syncthreads();
+  for (int l = threadIdx.x; l < C::T2; l += blockDim.x) {
+    const int i = l % NF, j = (l / NF) % NF, c = l / (NF * NF);
+    double s = 0.0;
+#pragma unroll
+    for (int b = 0; b < NC; ++b) s += I[j * NC + b] * t1[i + NF * (b + NC * c)];
+    t2[l] = s;
+  }
+  __syncthreads();
+  for (int l = threadIdx.x; l < C::NF3; l += blockDim.x) {
+    const int i = l % NF, j = (l / NF) % NF, k = l / (NF * NF);
+    if ((i == 0 && ex > 0) || (j == 0 && ey > 0) || (k == 0 && ez > 0)) continue;   // not the owner
+    const int I0 = ex * PF + i, J0 = ey * PF + j, K0 = ez * PF + k;
+    const bool bnd = I0 == 0 || I0 == mf.Mx - 1 || J0 == 0 || J0 == mf.My - 1 || K0 == 0 || K0 == mf.Mz - 1;
+    const long long g = I0 + (long long)mf.Mx * (J0 + (long long)mf.My * K0);
+    if (bnd) {
+      if (!add) uf[g] = 0.0;
+      continue;
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) s += I[k * NC + c] * t2[i + NF * (j + NF * c)];
+    if (add) uf[g] += s; else uf[g] = s;
+  }
+}
+
+template <int PC>
+__global__ void __launch_bounds__(256) k_restrict(MeshDev mc, MeshDev mf, const double* __restrict__ rf,
+                                                  double* __restrict__ rc) {
+  using C = XferCfg<PC>;
+  constexpr int NC = C::NC, NF = C::NF, PF = C::PF;
+  extern __shared__ double sm[];
+  double* sf = sm;             // [k][j][i]
+  double* t1 = sf + C::NF3;    // [k][j][a]
+  double* t2 = t1 + C::R1;     // [k][b][a]
+  const double* I = c_I[PC - 1];
+  const long long e = blockIdx.x;
+  int ex, ey, ez;
+  ecoords(mf, e, ex, ey, ez);
+  for (int l = threadIdx.x; l < C::NF3; l += blockDim.x) {
+    const int i = l % NF, j = (l / NF) % NF, k = l / (NF * NF);
+    double v = 0.0;
+    if (!((i == 0 && ex > 0) || (j == 0 && ey > 0) || (k == 0 && ez > 0))) {
+      const int I0 = ex * PF + i, J0 = ey * PF + j, K0 = ez * PF + k;
+      const bool bnd = I0 == 0 || I0 == mf.Mx - 1 || J0 == 0 || J0 == mf.My - 1 || K0 == 0 || K0 == mf.Mz - 1;
+      if (!bnd) v = rf[I0 + (long long)mf.Mx * (J0 + (long long)mf.My * K0)];
+    }
+    sf[l] = v;
+  }
+  __syncthreads();
+  for (int l = threadIdx.x; l < C::R1; l += blockDim.x) {
+    const int a = l % NC, r = l / NC;     // r = j + NF k
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < NF; ++i) s += I[i * NC + a] * sf[i + NF * r];
+    t1[l] = s;
+  }
+  __syncthreads();
+  for (int l = threadIdx.x; l < C::R2; l += blockDim.x) {
+    const int a = l % NC, b = (l / NC) % NC, k = l / (NC * NC);
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < NF; ++j) s += I[j * NC + b] * t1[a + NC * (j + NF * k)];
+    t2[l] = s;
+  }
+  __syncthreads();
+  for (int l = threadIdx.x; l < C::NC3; l += blockDim.x) {
+    const int a = l % NC, b = (l / NC) % NC, c = l / (NC * NC);
+    const int I0 = ex * PC + a, J0 = ey * PC + b, K0 = ez * PC + c;
+    const bool bnd = I0 == 0 || I0 == mc.Mx - 1 || J0 == 0 || J0 == mc.My - 1 || K0 == 0 || K0 == mc.Mz - 1;
+    if (bnd) continue;
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < NF; ++k) s += I[k * NC + c] * t2[a + NC * (b + NC * k)];
+    atomicAdd(rc + I0 + (long long)mc.Mx * (J0 + (long long)mc.My * K0), s);
+  }
+}
+
+template <int PC>
+static cudaError_t prolong_p(const MeshDev& mc, const MeshDev& mf, const double* uc, double* uf, int add,
+                             cudaStream_t s) {
+  using C = XferCfg<PC>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_prolong<PC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_P);
+    if (e) return e;
+    attr = true;
+  }
+  k_prolong<PC><<<(unsigned)mf.E, 256, C::SMEM_P, s>>>(mc, mf, uc, uf, add);
+  return cudaGetLastError();
+}
+
+template <int PC>
+static cudaError_t restrict_p(const MeshDev& mc, const MeshDev& mf, const double* rf, double* rc, cudaStream_t s) {
+  using C = XferCfg<PC>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_restrict<PC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_R);
+    if (e) return e;
+    attr = true;
+  }
+  cudaError_t e = cudaMemsetAsync(rc, 0, sizeof(double) * mc.N, s);
+  if (e) return e;
+  k_restrict<PC><<<(unsigned)mf.E, 256, C::SMEM_R, s>>>(mc, mf, rf, rc);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_prolong(const MeshDev& mc, const MeshDev& mf, const double* uc, double* uf, int add,
+                           cudaStream_t s) {
+  switch (mc.p) {
+    case 1: return prolong_p<1>(mc, mf, uc, uf, add, s);
+    case 2: return prolong_p<2>(mc, mf, uc, uf, add, s);
+    case 3: return prolong_p<3>(mc, mf, uc, uf, add, s);
+    case 4: return prolong_p<4>(mc, mf, uc, uf, add, s);
+    case 5: return prolong_p<5>(mc, mf, uc, uf, add, s);
+    case 6: return prolong_p<6>(mc, mf, uc, uf, add, s);
+    case 7: return prolong_p<7>(mc, mf, uc, uf, add, s);
+    case 8: return prolong_p<8>(mc, mf, uc, uf, add, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_restrict(const MeshDev& mc, const MeshDev& mf, const double* rf, double* rc, cudaStream_t s) {
+  switch (mc.p) {
+    case 1: return restrict_p<1>(mc, mf, rf, rc, s);
+    case 2: return restrict_p<2>(mc, mf, rf, rc, s);
+    case 3: return restrict_p<3>(mc, mf, rf, rc, s);
+    case 4: return restrict_p<4>(mc, mf, rf, rc, s);
+    case 5: return restrict_p<5>(mc, mf, rf, rc, s);
+    case 6: return restrict_p<6>(mc, mf, rf, rc, s);
+    case 7: return restrict_p<7>(mc, mf, rf, rc, s);
+    case 8: return restrict_p<8>(mc, mf, rf, rc, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace sfmg

@@ -1,0 +1,561 @@
+// C ABI of libsfmg (include/sfmg.h): argument checking, workspace carving, and the host-side
+// orchestration of the kernels (Chebyshev recurrence scalars, V-cycle recursion, Algorithm 1).
+// Host code only launches kernels on the caller's stream; no arithmetic of the method runs here
+// except the scalar Chebyshev recurrence coefficients (R7).
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "sfmg_internal.h"
+
+namespace sfmg {
+
+static thread_local std::string g_err;
+void set_error(const std::string& s) { g_err = s; }
+
+static sfmg_status cuda_fail(cudaError_t e, const char* where) {
+  set_error(std::string(where) + ": " + cudaGetErrorString(e));
+  return SFMG_E_CUDA;
+}
+
+#define CK(call)                                         \
+  do {                                                   \
+    cudaError_t e_ = (call);                             \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call);  \
+  } while (0)
+
+static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+static sfmg_status check_problem(const sfmg_problem* pr) {
+  if (!pr) { set_error("null problem"); return SFMG_E_ARG; }
+  if (pr->order < 1 || pr->order > kMaxOrder) { set_error("order must be 1..16"); return SFMG_E_ORDER; }
+  if (pr->nex < 1 || pr->ney < 1 || pr->nez < 1) { set_error("element counts must be >= 1"); return SFMG_E_MESH; }
+  long long Mx = (long long)pr->nex * pr->order + 1, My = (long long)pr->ney * pr->order + 1,
+            Mz = (long long)pr->nez * pr->order + 1;
+  if (Mx * My * Mz >= (1LL << 31)) { set_error("lattice exceeds 2^31 nodes"); return SFMG_E_MESH; }
+  if (pr->warp != 0 && pr->warp != 1) { set_error("warp must be 0 or 1"); return SFMG_E_ARG; }
+  if (pr->coeff < 0 || pr->coeff > 3) { set_error("coeff must be 0..3"); return SFMG_E_ARG; }
+  return SFMG_OK;
+}
+
+static MeshDev make_mesh(const sfmg_problem* pr) {
+  MeshDev m;
+  m.nex = pr->nex; m.ney = pr->ney; m.nez = pr->nez; m.p = pr->order;
+  m.Mx = pr->nex * pr->order + 1; m.My = pr->ney * pr->order + 1; m.Mz = pr->nez * pr->order + 1;
+  m.E = (long long)pr->nex * pr->ney * pr->nez;
+  m.N = (long long)m.Mx * m.My * m.Mz;
+  m.warp = pr->warp; m.coeff = pr->coeff;
+  m.amp = pr->warp_amp; m.c0 = pr->c0; m.c1 = pr->c1;
+  return m;
+}
+
+struct LevelLayout {
+  size_t G, dinv, y, t0, t1, t2, partials, scalars, counter, bad, total;
+};
+
+static LevelLayout level_layout(const MeshDev& m) {
+  LevelLayout L;
+  const long long n3 = (long long)(m.p + 1) * (m.p + 1) * (m.p + 1);
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off += align_up(bytes); return o; };
+  L.G = take(sizeof(double) * 6 * (size_t)m.E * n3);
+  L.dinv = take(sizeof(double) * m.N);
+  L.y = take(sizeof(double) * m.N);
+  L.t0 = take(sizeof(double) * m.N);
+  L.t1 = take(sizeof(double) * m.N);
+  L.t2 = take(sizeof(double) * m.N);
+  L.partials = take(sizeof(double) * kRedBlocks * kRedSlots);
+  L.scalars = take(sizeof(double) * 32);
+  L.counter = take(sizeof(unsigned int));
+  L.bad = take(sizeof(int));
+  L.total = off;
+  return L;
+}
+
+static sfmg_status level_build(const sfmg_problem* pr, void* d_ws, size_t ws_bytes, cudaStream_t s,
+                               sfmg_level_s** out) {
+  MeshDev m = make_mesh(pr);
+  LevelLayout L = level_layout(m);
+  if (!d_ws || ((uintptr_t)d_ws & 255) || ws_bytes < L.total) {
+    set_error("workspace too small or not 256-byte aligned");
+    return SFMG_E_WORKSPACE;
+  }
+  char* base = (char*)d_ws;
+  sfmg_level_s* lv = new (std::nothrow) sfmg_level_s();
+  if (!lv) { set_error("host allocation failed"); return SFMG_E_ARG; }
+  lv->prob = *pr; lv->m = m; lv->p = m.p; lv->n = m.p + 1;
+  lv->n3 = (long long)lv->n * lv->n * lv->n; lv->E = m.E; lv->N = m.N;
+  lv->G = (double*)(base + L.G);
+  lv->dinv = (double*)(base + L.dinv);
+  lv->y = (double*)(base + L.y);
+  lv->t0 = (double*)(base + L.t0);
+  lv->t1 = (double*)(base + L.t1);
+  lv->t2 = (double*)(base + L.t2);
+  lv->red.partials = (double*)(base + L.partials);
+  lv->red.scalars = (double*)(base + L.scalars);
+  lv->red.counter = (unsigned int*)(base + L.counter);
+  lv->bad = (int*)(base + L.bad);
+  lv->ws_bytes = L.total;
+  lv->owned_by_hier = false;
+  auto fail = [&](sfmg_status st) { delete lv; return st; };
+  cudaError_t e;
+  if ((e = upload_order_tables(m.p, s))) return fail(cuda_fail(e, "upload_order_tables"));
+  if ((e = cudaMemsetAsync(lv->red.counter, 0, sizeof(unsigned int), s))) return fail(cuda_fail(e, "memset"));
+  if ((e = cudaMemsetAsync(lv->bad, 0, sizeof(int), s))) return fail(cuda_fail(e, "memset"));
+  if ((e = launch_geometry(m, lv->G, lv->bad, s))) return fail(cuda_fail(e, "geometry"));
+  int bad = 0;
+  if ((e = cudaMemcpyAsync(&bad, lv->bad, sizeof(int), cudaMemcpyDeviceToHost, s))) return fail(cuda_fail(e, "copy"));
+  if ((e = cudaStreamSynchronize(s))) return fail(cuda_fail(e, "geometry sync"));
+  if (bad > 0) {
+    set_error("det J <= 0 at " + std::to_string(bad) + " quadrature points");
+    return fail(SFMG_E_GEOMETRY);
+  }
+  if ((e = launch_diag(m, 0, lv->G, lv->t0, s))) return fail(cuda_fail(e, "diag"));
+  if ((e = launch_recip(lv->t0, lv->dinv, m.N, s))) return fail(cuda_fail(e, "recip"));
+  *out = lv;
+  return SFMG_OK;
+}
+
+// y <- A_D u (bc 0) or A u (bc 1): boundary/zero init then the element kernel
+static cudaError_t op_apply(sfmg_level_s* lv, int bc, const double* u, double* v, cudaStream_t s) {
+  cudaError_t e = launch_init(lv->m, bc, u, 0.0, v, s);
+  if (e) return e;
+  return launch_apply(lv->m, bc, lv->G, u, v, s);
+}
+
+// Degree-K Chebyshev application, iterate form of R7:
+//   x1 = x0 + (1/theta) D^{-1} (b - A x0)
+//   x_{k+1} = x_k + rho_k rho_{k-1} (x_k - x_{k-1}) + (2 rho_k / delta) D^{-1} (b - A x_k)
+// with rho_0 = 1/sigma, rho_k = 1/(2 sigma - rho_{k-1}), sigma = theta/delta.  K applies.
+static cudaError_t op_cheb(sfmg_level_s* lv, const double* b, double* x, int K, double lo, double hi,
+                           cudaStream_t s) {
+  const double theta = 0.5 * (hi + lo), delta = 0.5 * (hi - lo), sigma = theta / delta;
+  double rho_prev = 1.0 / sigma;
+  cudaError_t e = op_apply(lv, 0, x, lv->y, s);
+  if (e) return e;
+  double* A = x;
+  double* B = lv->t0;
+  double* cur = A;
+  double* prev = nullptr;
+  for (int k = 0; k < K; ++k) {
+    double c1 = 0.0, c2 = 1.0 / theta;
+    if (k > 0) {
+      const double rho = 1.0 / (2.0 * sigma - rho_prev);
+      c1 = rho * rho_prev;
+      c2 = 2.0 * rho / delta;
+      rho_prev = rho;
+    }
+    double* out = (k == K - 1) ? A : (k == 0 ? B : prev);
+    if (k > 0) {
+      e = launch_apply(lv->m, 0, lv->G, cur, lv->y, s);   // y was re-initialised by the last update
+      if (e) return e;
+    }
+    e = launch_cheb_update(lv->m, cur, prev ? prev : cur, out, b, lv->y, lv->dinv, c1, c2, s);
+    if (e) return e;
+    prev = cur;
+    cur = out;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace sfmg
+
+using namespace sfmg;
+
+extern "C" {
+
+const char* sfmg_version(void) { return "sfmg 0.1 (sm_100a, fp64)"; }
+const char* sfmg_last_error(void) { return g_err.c_str(); }
+
+sfmg_status sfmg_level_query(const sfmg_problem* prob, int64_t* n_dofs, int64_t* n_elem, size_t* ws_bytes) {
+  sfmg_status st = check_problem(prob);
+  if (st) return st;
+  MeshDev m = make_mesh(prob);
+  if (n_dofs) *n_dofs = m.N;
+  if (n_elem) *n_elem = m.E;
+  if (ws_bytes) *ws_bytes = level_layout(m).total;
+  return SFMG_OK;
+}
+
+sfmg_status sfmg_level_create(const sfmg_problem* prob, void* d_ws, size_t ws_bytes, void* stream, sfmg_level* out) {
+  sfmg_status st = check_problem(prob);
+  if (st) return st;
+  if (!out) { set_error("null output handle"); return SFMG_E_ARG; }
+  return level_build(prob, d_ws, ws_bytes, (cudaStream_t)stream, out);
+}
+
+sfmg_status sfmg_level_destroy(sfmg_level lv) {
+  if (!lv) return SFMG_E_ARG;
+  if (lv->owned_by_hier) { set_error("level is owned by a hierarchy"); return SFMG_E_ARG; }
+  delete lv;
+  return SFMG_OK;
+}
+
+sfmg_status sfmg_level_info(sfmg_level lv, int64_t* n_dofs, int64_t* n_elem, int32_t* order) {
+  if (!lv) return SFMG_E_ARG;
+  if (n_dofs) *n_dofs = lv->N;
+  if (n_elem) *n_elem = lv->E;
+  if (order) *order = lv->p;
+  return SFMG_OK;
+}
+
+sfmg_status sfmg_export_l2g(sfmg_level lv, int32_t* d_l2g, void* stream) {
+  if (!lv || !d_l2g) return SFMG_E_ARG;
+  CK(launch_export_maps(lv->m, d_l2g, nullptr, nullptr, (cudaStream_t)stream));
+  return SFMG_OK;
+}
+sfmg_status sfmg_export_mask(sfmg_level lv, uint8_t* d_mask, void* stream) {
+  if (!lv || !d_mask) return SFMG_E_ARG;
+  CK(launch_export_maps(lv->m, nullptr, d_mask, nullptr, (cudaStream_t)stream));
+  return SFMG_OK;
+}
+sfmg_status sfmg_export_colors(sfmg_level lv, uint8_t* d_col, void* stream) {
+  if (!lv || !d_col) return SFMG_E_ARG;
+  CK(launch_export_maps(lv->m, nullptr, nullptr, d_col, (cudaStream_t)stream));
+  return SFMG_OK;
+}
+sfmg_status sfmg_export_geometry(sfmg_level lv, double* d_G, void* stream) {
+  if (!lv || !d_G) return SFMG_E_ARG;
+  CK(cudaMemcpyAsync(d_G, lv->G, sizeof(double) * 6 * lv->E * lv->n3, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+  return SFMG_OK;
+}
+
+sfmg_status sfmg_apply(sfmg_level lv, int32_t bc, const double* d_u, double* d_v, int64_t n, void* stream) {
+  if (!lv || !d_u || !d_v || d_u == d_v || (bc != 0 && bc != 1)) { set_error("bad argument to sfmg_apply"); return SFMG_E_ARG; }
+  if (n != lv->N) { set_error("vector length != N"); return SFMG_E_ARG; }
+  CK(op_apply(lv, bc, d_u, d_v, (cudaStream_t)stream));
+  return SFMG_OK;
+}
+
+sfmg_status sfmg_diag(sfmg_level lv, int32_t bc, double* d_diag, int64_t n, void* stream) {
+  if (!lv || !d_diag || (bc != 0 && bc != 1)) return SFMG_E_ARG;
+  if (n != lv->N) { set_error("vector length != N"); return SFMG_E_ARG; }
+  CK(launch_diag(lv->m, bc, lv->G, d_diag, (cudaStream_t)stream));
+  return SFMG_OK;
+}
+
+sfmg_status sfmg_lambda_max(sfmg_level lv, int32_t iters, uint64_t seed, double* h_lambda, void* stream) {
+  if (!lv || !h_lambda || iters < 1) return SFMG_E_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  double* x = lv->t1;
+  double* y = lv->y;
+  CK(launch_power_start(lv->m, seed, x, y, s));
+  for (int it = 0; it < iters; ++it) {
+    CK(launch_apply(lv->m, 0, lv->G, x, y, s));
+    CK(launch_power_step(lv->m, lv->red, x, y, lv->dinv, s));
+  }
+  CK(cudaMemcpyAsync(h_lambda, lv->red.scalars + 3, sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return SFMG_OK;
+}
+
+sfmg_status sfmg_cheb(sfmg_level lv, const double* d_b, double* d_x, int64_t n, int32_t degree, double lam_lo,
+                      double lam_hi, void* stream) {
+  if (!lv || !d_b || !d_x || degree < 1 || !(lam_hi > lam_lo) || !(lam_lo > 0.0)) {
+    set_error("bad argument to sfmg_cheb");
+    return SFMG_E_ARG;
+  }
+  if (n != lv->N) { set_error("vector length != N"); return SFMG_E_ARG; }
+  CK(op_cheb(lv, d_b, d_x, degree, lam_lo, lam_hi, (cudaStream_t)stream));
+  return SFMG_OK;
+}
+
+sfmg_status sfmg_load_vector(sfmg_level lv, int32_t rhs_id, double* d_f, int64_t n, void* stream) {
+  if (!lv || !d_f || rhs_id != 1) return SFMG_E_ARG;
+  if (n != lv->N) return SFMG_E_ARG;
+  CK(launch_load(lv->m, rhs_id, d_f, (cudaStream_t)stream));
+  return SFMG_OK;
+}
+
+sfmg_status sfmg_apply_host(sfmg_level lv, int32_t bc, const double* h_u, double* h_v, int64_t n, void* stream) {
+  if (!lv || !h_u || !h_v || (bc != 0 && bc != 1)) return SFMG_E_ARG;
+  if (n != lv->N) return SFMG_E_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t bytes = sizeof(double) * lv->N;
+  CK(cudaMemcpyAsync(lv->t1, h_u, bytes, cudaMemcpyHostToDevice, s));
+  CK(op_apply(lv, bc, lv->t1, lv->t2, s));
+  CK(cudaMemcpyAsync(h_v, lv->t2, bytes, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return SFMG_OK;
+}
+
+sfmg_status sfmg_cheb_host(sfmg_level lv, const double* h_b, double* h_x, int64_t n, int32_t degree, double lam_lo,
+                           double lam_hi, void* stream) {
+  if (!lv || !h_b || !h_x || degree < 1 || !(lam_hi > lam_lo) || !(lam_lo > 0.0)) return SFMG_E_ARG;
+  if (n != lv->N) return SFMG_E_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t bytes = sizeof(double) * lv->N;
+  CK(cudaMemcpyAsync(lv->t1, h_b, bytes, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(lv->t2, h_x, bytes, cudaMemcpyHostToDevice, s));
+  CK(op_cheb(lv, lv->t1, lv->t2, degree, lam_lo, lam_hi, s));
+  CK(cudaMemcpyAsync(h_x, lv->t2, bytes, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return SFMG_OK;
+}
+
+static sfmg_status check_pair(sfmg_level c, sfmg_level f) {
+  if (!c || !f) return SFMG_E_ARG;
+  if (f->p != 2 * c->p || f->m.nex != c->m.nex || f->m.ney != c->m.ney || f->m.nez != c->m.nez || c->p > 8) {
+    set_error("levels are not (p/2, p) on one element grid");
+    return SFMG_E_PCOARSEN;
+  }
+  return SFMG_OK;
+}
+
+sfmg_status sfmg_prolong(sfmg_level coarse, sfmg_level fine, const double* d_uc, double* d_uf, void* stream) {
+  sfmg_status st = check_pair(coarse, fine);
+  if (st) return st;
+  if (!d_uc || !d_uf) return SFMG_E_ARG;
+  CK(upload_interp_tables(coarse->p, (cudaStream_t)stream));
+  CK(launch_prolong(coarse->m, fine->m, d_uc, d_uf, 0, (cudaStream_t)stream));
+  return SFMG_OK;
+}
+
+sfmg_status sfmg_restrict(sfmg_level coarse, sfmg_level fine, const double* d_rf, double* d_rc, void* stream) {
+  sfmg_status st = check_pair(coarse, fine);
+  if (st) return st;
+  if (!d_rf || !d_rc) return SFMG_E_ARG;
+  CK(upload_interp_tables(coarse->p, (cudaStream_t)stream));
+  CK(launch_restrict(coarse->m, fine->m, d_rf, d_rc, (cudaStream_t)stream));
+  return SFMG_OK;
+}
+
+// ------------------------------------------------------------------------------ hierarchy
+
+static sfmg_status hier_orders(const sfmg_problem* fine, std::vector<int>& orders) {
+  orders.clear();
+  for (int q = fine->order;; q /= 2) {
+    orders.push_back(q);
+    if (q == 1) break;
+    if (q % 2) { set_error("order cannot be p-coarsened to 1 by halving"); return SFMG_E_PCOARSEN; }
+  }
+  return SFMG_OK;
+}
+
+static sfmg_status check_mg(const sfmg_mg_params* mg) {
+  if (!mg || mg->nu_pre < 0 || mg->nu_post < 0 || mg->cheb_degree < 1 || !(mg->eig_hi_frac > mg->eig_lo_frac) ||
+      !(mg->eig_lo_frac > 0) || mg->power_iters < 1 || !(mg->coarse_rtol > 0) || mg->coarse_max_iter < 1) {
+    set_error("bad multigrid parameters");
+    return SFMG_E_ARG;
+  }
+  return SFMG_OK;
+}
+
+sfmg_status sfmg_hier_query(const sfmg_problem* fine, const sfmg_mg_params* mg, size_t* ws_bytes) {
+  sfmg_status st = check_problem(fine);
+  if (st) return st;
+  if ((st = check_mg(mg))) return st;
+  std::vector<int> orders;
+  if ((st = hier_orders(fine, orders))) return st;
+  size_t total = 0;
+  for (size_t l = 0; l < orders.size(); ++l) {
+    sfmg_problem q = *fine;
+    q.order = orders[l];
+    MeshDev m = make_mesh(&q);
+    total += level_layout(m).total + 3 * align_up(sizeof(double) * m.N);
+    if (l == 0) total += 4 * align_up(sizeof(double) * m.N);
+  }
+  if (ws_bytes) *ws_bytes = total;
+  return SFMG_OK;
+}
+
+sfmg_status sfmg_hier_destroy(sfmg_hier h) {
+  if (!h) return SFMG_E_ARG;
+  for (sfmg_level_s* lv : h->lv) delete lv;
+  delete h;
+  return SFMG_OK;
+}
+
+sfmg_status sfmg_hier_create(const sfmg_problem* fine, const sfmg_mg_params* mg, void* d_ws, size_t ws_bytes,
+                             void* stream, sfmg_hier* out) {
+  size_t need = 0;
+  sfmg_status st = sfmg_hier_query(fine, mg, &need);
+  if (st) return st;
+  if (!out) return SFMG_E_ARG;
+  if (!d_ws || ((uintptr_t)d_ws & 255) || ws_bytes < need) { set_error("workspace too small"); return SFMG_E_WORKSPACE; }
+  cudaStream_t s = (cudaStream_t)stream;
+  std::vector<int> orders;
+  hier_orders(fine, orders);
+  sfmg_hier_s* h = new sfmg_hier_s();
+  h->mg = *mg;
+  h->fine_applies = 0;
+  char* base = (char*)d_ws;
+  for (size_t l = 0; l < orders.size(); ++l) {
+    sfmg_problem q = *fine;
+    q.order = orders[l];
+    MeshDev m = make_mesh(&q);
+    LevelLayout L = level_layout(m);
+    sfmg_level_s* lv = nullptr;
+    st = level_build(&q, base, L.total, s, &lv);
+    if (st) { sfmg_hier_destroy(h); return st; }
+    lv->owned_by_hier = true;
+    h->lv.push_back(lv);
+    base += L.total;
+    const size_t vb = align_up(sizeof(double) * m.N);
+    h->b.push_back((double*)base); base += vb;
+    h->x.push_back((double*)base); base += vb;
+    h->r.push_back((double*)base); base += vb;
+    if (l == 0) {
+      h->pr = (double*)base; base += vb;
+      h->pz = (double*)base; base += vb;
+      h->pp = (double*)base; base += vb;
+      h->ph = (double*)base; base += vb;
+    }
+    if (orders[l] > 1) {
+      cudaError_t e = upload_interp_tables(orders[l] / 2, s);
+      if (e) { sfmg_hier_destroy(h); return cuda_fail(e, "interp tables"); }
+    }
+  }
+  h->lam.assign(h->lv.size(), 0.0);
+  for (size_t l = 0; l + 1 < h->lv.size(); ++l) {
+    double lam = 0.0;
+    st = sfmg_lambda_max(h->lv[l], mg->power_iters, mg->power_seed, &lam, stream);
+    if (st) { sfmg_hier_destroy(h); return st; }
+    h->lam[l] = lam;
+  }
+  *out = h;
+  return SFMG_OK;
+}
+
+sfmg_status sfmg_hier_info(sfmg_hier h, int32_t* n_levels, int64_t* n_dofs_fine) {
+  if (!h) return SFMG_E_ARG;
+  if (n_levels) *n_levels = (int32_t)h->lv.size();
+  if (n_dofs_fine) *n_dofs_fine = h->lv[0]->N;
+  return SFMG_OK;
+}
+
+sfmg_status sfmg_hier_level(sfmg_hier h, int32_t l, sfmg_level* out) {
+  if (!h || !out || l < 0 || l >= (int32_t)h->lv.size()) return SFMG_E_ARG;
+  *out = h->lv[l];
+  return SFMG_OK;
+}
+
+sfmg_status sfmg_hier_lambda(sfmg_hier h, int32_t l, double* lam) {
+  if (!h || !lam || l < 0 || l >= (int32_t)h->lv.size()) return SFMG_E_ARG;
+  *lam = h->lam[l];
+  return SFMG_OK;
+}
+
+}  // extern "C"
+
+namespace sfmg {
+
+static cudaError_t vcycle_level(sfmg_hier_s* h, size_t l, const double* b, double* x, cudaStream_t s) {
+  sfmg_level_s* lv = h->lv[l];
+  const sfmg_mg_params& mg = h->mg;
+  cudaError_t e;
+  if (l + 1 == h->lv.size()) {
+    return launch_coarse_cg(lv->m, lv->G, b, x, lv->t0, lv->t1, lv->y, lv->red.scalars, mg.coarse_rtol,
+                            mg.coarse_max_iter, s);
+  }
+  const double lo = mg.eig_lo_frac * h->lam[l], hi = mg.eig_hi_frac * h->lam[l];
+  if ((e = cudaMemsetAsync(x, 0, sizeof(double) * lv->N, s))) return e;
+  for (int i = 0; i < mg.nu_pre; ++i) {
+    if ((e = op_cheb(lv, b, x, mg.cheb_degree, lo, hi, s))) return e;
+    if (l == 0) h->fine_applies += mg.cheb_degree;
+  }
+  if ((e = op_apply(lv, 0, x, lv->y, s))) return e;
+  if (l == 0) h->fine_applies += 1;
+  if ((e = launch_residual(b, lv->y, h->r[l], lv->N, s))) return e;
+  sfmg_level_s* c = h->lv[l + 1];
+  if ((e = launch_restrict(c->m, lv->m, h->r[l], h->b[l + 1], s))) return e;
+  if ((e = vcycle_level(h, l + 1, h->b[l + 1], h->x[l + 1], s))) return e;
+  if ((e = launch_prolong(c->m, lv->m, h->x[l + 1], x, 1, s))) return e;
+  for (int i = 0; i < mg.nu_post; ++i) {
+    if ((e = op_cheb(lv, b, x, mg.cheb_degree, lo, hi, s))) return e;
+    if (l == 0) h->fine_applies += mg.cheb_degree;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace sfmg
+
+extern "C" {
+
+sfmg_status sfmg_vcycle(sfmg_hier h, const double* d_b, double* d_x, void* stream) {
+  if (!h || !d_b || !d_x || d_b == d_x) return SFMG_E_ARG;
+  CK(vcycle_level(h, 0, d_b, d_x, (cudaStream_t)stream));
+  return SFMG_OK;
+}
+
+sfmg_status sfmg_solve(sfmg_hier h, int32_t mode, const double* d_b, double* d_x, double rtol, int32_t max_iter,
+                       sfmg_report* rep, void* stream) {
+  if (!h || !d_b || !d_x || (mode != 0 && mode != 1) || !(rtol > 0) || max_iter < 0) return SFMG_E_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  sfmg_level_s* lv = h->lv[0];
+  const long long N = lv->N;
+  double* sc = lv->red.scalars;
+  h->fine_applies = 0;
+  int64_t vcycles = 0;
+  CK(cudaMemsetAsync(d_x, 0, sizeof(double) * N, s));
+  CK(cudaMemcpyAsync(h->pr, d_b, sizeof(double) * N, cudaMemcpyDeviceToDevice, s));
+  CK(launch_dot(lv->red, h->pr, h->pr, N, 7, s));
+  double host[2] = {0, 0};
+  CK(cudaMemcpyAsync(host, sc + 7, sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const double r0 = std::sqrt(host[0]);
+  double rn = r0;
+  int it = 0, converged = 0;
+  sfmg_status result = SFMG_OK;
+  if (rep && rep->history && rep->history_cap > 0) rep->history[0] = r0;
+  if (r0 == 0.0) {
+    converged = 1;
+  } else if (mode == 0) {
+    while (it < max_iter) {
+      if (rn <= rtol * r0) { converged = 1; break; }
+      if (rn > 10.0 * r0) break;
+      CK(vcycle_level(h, 0, h->pr, h->pz, s));
+      ++vcycles;
+      CK(launch_axpy1(d_x, h->pz, N, s));
+      CK(op_apply(lv, 0, d_x, h->ph, s));
+      h->fine_applies += 1;
+      CK(launch_residual(d_b, h->ph, h->pr, N, s));
+      CK(launch_dot(lv->red, h->pr, h->pr, N, 7, s));
+      CK(cudaMemcpyAsync(host, sc + 7, sizeof(double), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      rn = std::sqrt(host[0]);
+      ++it;
+      if (rep && rep->history && it < rep->history_cap) rep->history[it] = rn;
+    }
+    if (rn <= rtol * r0) converged = 1;
+  } else {
+    // Algorithm 1 with slots: 12/13 rho_r (alternating), 6 (p,h), 7 |r|^2
+    int sa = 12, sb = 13;
+    CK(vcycle_level(h, 0, h->pr, h->pz, s));
+    ++vcycles;
+    CK(launch_copy(h->pz, h->pp, N, s));
+    CK(launch_dot(lv->red, h->pz, h->pr, N, sa, s));
+    while (it < max_iter) {
+      CK(op_apply(lv, 0, h->pp, h->ph, s));                       // h = A p
+      h->fine_applies += 1;
+      CK(launch_dot(lv->red, h->pp, h->ph, N, 6, s));              // (p, h)
+      CK(launch_pcg_xr(lv->red, d_x, h->pr, h->pp, h->ph, sa, 6, 7, N, s));  // u += a p, r -= a h
+      CK(cudaMemcpyAsync(host, sc + 6, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      ++it;
+      if (!(host[0] > 0.0)) { result = SFMG_E_BREAKDOWN; set_error("(p, A p) <= 0 in CG"); break; }
+      rn = std::sqrt(host[1]);
+      if (rep && rep->history && it < rep->history_cap) rep->history[it] = rn;
+      if (rn <= rtol * r0) { converged = 1; break; }                // convergence test
+      if (rn > 10.0 * r0) break;
+      CK(vcycle_level(h, 0, h->pr, h->pz, s));                     // rho = M r
+      ++vcycles;
+      CK(launch_dot(lv->red, h->pz, h->pr, N, sb, s));             // (rho, r)
+      CK(launch_pcg_p(lv->red, h->pp, h->pz, sb, sa, N, s));       // p = rho + beta p
+      std::swap(sa, sb);
+    }
+  }
+  if (rep) {
+    rep->iterations = it;
+    rep->converged = converged;
+    rep->r0_norm = r0;
+    rep->r_norm = rn;
+    rep->fine_applies = h->fine_applies;
+    rep->vcycles = vcycles;
+  }
+  return result;
+}
+
+}  // extern "C"

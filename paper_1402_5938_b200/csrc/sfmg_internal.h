@@ -1,0 +1,122 @@
+// Internal declarations of libsfmg (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "sfmg.h"
+
+namespace sfmg {
+
+constexpr int kMaxOrder = 16;
+constexpr int kRedBlocks = 592;   // 4 x 148 SMs: fixed grid of the deterministic reductions
+constexpr int kRedSlots = 4;      // partial sums per reduction pass
+
+// Mesh + problem description passed by value to kernels.
+struct MeshDev {
+  int nex, ney, nez, p;
+  int Mx, My, Mz;          // lattice sizes (nex p + 1, ...)
+  long long E, N;          // elements, dofs
+  int warp, coeff;
+  double amp, c0, c1;
+};
+
+// Device reduction scratch: partials[kRedBlocks][kRedSlots], scalars[32], counter.
+struct RedScratch {
+  double* partials;
+  double* scalars;
+  unsigned int* counter;
+};
+
+// 1-D tables of one order (host), sizes n, n*n.
+struct Basis1D {
+  int p = 0, n = 0;
+  std::vector<double> x, w, D;   // D[i*n+m] = ell_m'(x_i)
+};
+Basis1D make_basis(int p);
+// I[i*(pc+1)+a] = ell^{pc}_a(x^{pf}_i)
+std::vector<double> make_interp(int pc, int pf);
+
+}  // namespace sfmg
+
+struct sfmg_level_s {
+  sfmg_problem prob;
+  sfmg::MeshDev m;
+  int p, n;
+  long long n3, E, N;
+  // views into the caller's workspace
+  double* G;       // [E][6][n3]
+  double* dinv;    // [N] 1/diag(A_D)
+  double* y;       // [N] operator output scratch
+  double* t0;      // [N] scratch (Chebyshev previous iterate, host-variant staging)
+  double* t1;      // [N] scratch (power iterate, host-variant staging)
+  double* t2;      // [N] scratch (host-variant staging)
+  sfmg::RedScratch red;
+  int* bad;        // geometry check counter
+  size_t ws_bytes;
+  bool owned_by_hier;
+};
+
+struct sfmg_hier_s {
+  sfmg_mg_params mg;
+  std::vector<sfmg_level_s*> lv;
+  std::vector<double> lam;
+  std::vector<double*> b, x, r;  // per-level V-cycle vectors
+  double *pr, *pz, *pp, *ph;     // PCG vectors on the finest level
+  int64_t fine_applies;
+};
+
+namespace sfmg {
+
+// ---- launchers (k_operator.cu)
+cudaError_t upload_order_tables(int p, cudaStream_t s);
+cudaError_t launch_geometry(const MeshDev& m, double* G, int* bad, cudaStream_t s);
+// v = bnd ? (u ? u[g] : bval) : 0  (bc 0);  v = 0  (bc 1)
+cudaError_t launch_init(const MeshDev& m, int bc, const double* u, double bval, double* v, cudaStream_t s);
+// v += A(M u) on interior rows (bc 0) or all rows (bc 1); v must be initialised
+cudaError_t launch_apply(const MeshDev& m, int bc, const double* G, const double* u, double* v, cudaStream_t s);
+cudaError_t launch_diag(const MeshDev& m, int bc, const double* G, double* d, cudaStream_t s);
+cudaError_t launch_load(const MeshDev& m, int rhs_id, double* f, cudaStream_t s);
+// out = cur + c1 (cur - prev) + c2 dinv (b - y); then y = bnd ? out : 0 (ready for next apply)
+cudaError_t launch_cheb_update(const MeshDev& m, const double* cur, const double* prev, double* out,
+                               const double* b, double* y, const double* dinv, double c1, double c2,
+                               cudaStream_t s);
+cudaError_t launch_export_maps(const MeshDev& m, int32_t* l2g, uint8_t* mask, uint8_t* col, cudaStream_t s);
+// single-CTA CG on a (small) level: x = A_D^{-1} b to rtol (R13)
+cudaError_t launch_coarse_cg(const MeshDev& m, const double* G, const double* b, double* x, double* r,
+                             double* p, double* q, double* scal, double rtol, int maxit, cudaStream_t s);
+
+// ---- vector kernels (k_blas.cu)
+cudaError_t launch_recip(const double* d, double* dinv, long long n, cudaStream_t s);
+cudaError_t launch_fill(double* x, double v, long long n, cudaStream_t s);
+cudaError_t launch_copy(const double* a, double* b, long long n, cudaStream_t s);
+// scalars[slot] = sum a.b (deterministic two-level reduction)
+cudaError_t launch_dot(const RedScratch& r, const double* a, const double* b, long long n, int slot, cudaStream_t s);
+// power iteration: scalars[0] = x.y, scalars[1] = x.x/dinv, scalars[2] = |y dinv|^2; then
+// x = y dinv / sqrt(scalars[2]); y = bnd ? x : 0; scalars[3] = scalars[0]/scalars[1]
+cudaError_t launch_power_step(const MeshDev& m, const RedScratch& r, double* x, double* y, const double* dinv,
+                              cudaStream_t s);
+cudaError_t launch_power_start(const MeshDev& m, uint64_t seed, double* x, double* y, cudaStream_t s);
+// r = b - y
+cudaError_t launch_residual(const double* b, const double* y, double* r, long long n, cudaStream_t s);
+// x += a p ; r -= a h with a = scal[ia] / scal[ib]; scalars[slot] = |r|^2
+cudaError_t launch_pcg_xr(const RedScratch& red, double* x, double* r, const double* p, const double* h,
+                          int ia, int ib, int slot, long long n, cudaStream_t s);
+// p = z + (scal[ia] / scal[ib]) p
+cudaError_t launch_pcg_p(const RedScratch& red, double* p, const double* z, int ia, int ib, long long n,
+                         cudaStream_t s);
+// x += y
+cudaError_t launch_axpy1(double* x, const double* y, long long n, cudaStream_t s);
+
+// ---- transfer (k_transfer.cu)
+cudaError_t upload_interp_tables(int pc, cudaStream_t s);
+// uf = P0 uc (add = 0) or uf += P0 uc (add = 1)
+cudaError_t launch_prolong(const MeshDev& mc, const MeshDev& mf, const double* uc, double* uf, int add,
+                           cudaStream_t s);
+// rc = P0^T rf (rc zeroed inside)
+cudaError_t launch_restrict(const MeshDev& mc, const MeshDev& mf, const double* rf, double* rc, cudaStream_t s);
+
+void set_error(const std::string& s);
+
+}  // namespace sfmg
