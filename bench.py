@@ -1,0 +1,386 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 hot path (BASELINE.json metric: fp64 matrix-free A.u GDoF/s vs roofline
+for p = 1..16; Chebyshev-Jacobi step time).
+
+Default (N=1): BASELINE config 2 (configs[1]) -- 16^3 deformed hexes, p = 8, mu = exp(3S),
+u uniform in [-1,1] from seed 1.  One step = one A_D u apply + one degree-4 Chebyshev-Jacobi
+application (b = 0, x0 = u, R16) = 5 operator applies.  `value` = N / (mean apply time) in GDoF/s.
+Between timed steps the L2 is flushed (a 512 MB write).  Extra keys report the config-3 p-sweep,
+config 4 (135 M dofs) and the config-5 p-MG preconditioned CG solve measured in the same run.
+
+Launch: python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+(N > 1 under torch.distributed.run: independent replicas, one per GPU -- DESIGN.md "replicas only").
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from paper_1402_5938_b200 import inputs  # noqa: E402
+
+METRIC = "fp64 matrix-free A.u GDoF/s (BASELINE config 2: 16^3 deformed hexes, p=8, mu=exp(3S))"
+UNIT = "GDoF/s"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            mp = json.load(fh)
+        return float(mp["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def algorithmic(d):
+    """apply bytes = 48 E n^3 (G) + 16 N (u read once, v written once);
+    Chebyshev step bytes = 48 E n^3 + 40 N; apply flops = E (12 n^4 + 15 n^3)."""
+    n = d["p"] + 1
+    E = d["nex"] * d["ney"] * d["nez"]
+    N = inputs.ndofs(d)
+    return dict(N=N, E=E, n=n, apply_bytes=48 * E * n ** 3 + 16 * N, step_bytes=48 * E * n ** 3 + 40 * N,
+                apply_flops=E * (12 * n ** 4 + 15 * n ** 3))
+
+
+# ------------------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join("/tmp", "sfmg_clocks_%d.csv" % os.getpid())
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + q,
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.fh.close()
+
+    def summary(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = []
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 9:
+                rows.append(f)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "samples": len(rows), "reasons": reasons}
+
+
+# ------------------------------------------------------------------------------------------ oracle (CPU)
+def oracle_apply_sample(d, seed, target_s=10.0):
+    """Time the oracle's O2 direct-quadrature apply (as it stands) over a bounded, evenly spaced sample
+    of the workload's elements with geometric factors precomputed; returns GDoF/s-equivalent
+    (N/E dofs per element), cores used and a description of the sample."""
+    import oracle
+    oracle.build()
+    L = oracle.Level(d["nex"], d["ney"], d["nez"], d["p"], d.get("warp", 0), d.get("amp", 0.0), d.get("coeff", 0),
+                     d.get("c0", 1.0), d.get("c1", 0.0), eager=False, geom_tier=2, tier=2)
+    u = inputs.uniform_pm1(seed, L.N)
+    ne = 16
+    while True:     # grow the sample until one pass costs ~target_s / 4 wall seconds
+        el = (np.arange(ne, dtype=np.int64) * max(1, L.E // ne)) % L.E
+        L.cache_elements(el)
+        t0 = time.perf_counter()
+        L.apply_elements(u, el, tier=2)
+        dt = time.perf_counter() - t0
+        if dt > target_s / 4 or ne >= L.E:
+            break
+        ne = min(L.E, ne * 4)
+    reps, tot = 0, 0.0
+    while tot < target_s * 0.75 and reps < 50:
+        t0 = time.perf_counter()
+        L.apply_elements(u, el, tier=2)
+        tot += time.perf_counter() - t0
+        reps += 1
+    per_elem = tot / reps / ne
+    gdofs = (L.N / L.E) / per_elem / 1e9
+    return gdofs, oracle.get_threads(), ("O2 apply over %d of %d elements (evenly spaced), %d reps, G precomputed; "
+                                         "GDoF/s scaled by N/E dofs per element" % (ne, L.E, reps))
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the oracle as the reference arm (tier: no reference implementation exists)."""
+    if rank != 0:
+        return 0
+    d = inputs.CONFIG2
+    import oracle
+    oracle.build()
+    L = oracle.Level(d["nex"], d["ney"], d["nez"], d["p"], d["warp"], d["amp"], d["coeff"], d["c0"], d["c1"],
+                     eager=False, geom_tier=2, tier=2)
+    u = inputs.uniform_pm1(1, L.N)
+    ne = 64
+    el = (np.arange(ne, dtype=np.int64) * (L.E // ne)) % L.E
+    L.cache_elements(el)
+    times = []
+    for k in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        L.apply_elements(u, el, tier=2)
+        dt = time.perf_counter() - t0
+        if k >= args.warmup:
+            times.append(dt)
+    per_step = sum(times) / len(times)
+    value = (L.N / L.E) * ne / per_step / 1e9
+    sample = "per step: O2 apply over %d of %d config-2 elements, G precomputed; GDoF/s scaled by N/E" % (ne, L.E)
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step * 1e3, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": "BASELINE config 2 (16^3 deformed hexes, p=8, mu=exp(3S), seed 1)",
+                      "sample": sample},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.get_threads(), "kind": "oracle",
+                            "sample": sample},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------------------------ GPU arm
+def run_gpu(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local_rank)
+    from paper_1402_5938_b200 import sfmg
+
+    dev = torch.device("cuda", local_rank)
+    stream = torch.cuda.current_stream()
+    hbm_peak, peak_kind = peaks()
+    flush = torch.empty(512 * 2 ** 20 // 4, dtype=torch.float32, device=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---------------- main workload: config 2
+    d = inputs.CONFIG2
+    alg = algorithmic(d)
+    lv = sfmg.Level(sfmg.Problem.from_dict(d), device=dev)
+    N = lv.N
+    u_host = torch.from_numpy(inputs.uniform_pm1(inputs.SEEDS[2], N)).pin_memory()
+    u = u_host.to(dev, non_blocking=True)
+    v = torch.empty_like(u)
+    b = torch.zeros_like(u)
+    x = torch.empty_like(u)
+    lam = lv.lambda_max(10, inputs.POWER_SEED)
+    lo, hi = 0.1 * lam, 1.1 * lam
+    launches_per_step = 2 + 5 + 4     # apply: init + element kernel; cheb(4): init + 4 element + 4 update
+
+    def step(ev):
+        ev[0].record(stream)
+        lv.apply(u, v)
+        ev[1].record(stream)
+        x.copy_(u)
+        ev[2].record(stream)
+        lv.cheb(b, x, 4, lo, hi)
+        ev[3].record(stream)
+
+    for _ in range(max(3, args.warmup)):
+        step([torch.cuda.Event(enable_timing=True) for _ in range(4)])
+    barrier()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        for k in range(args.steps):
+            flush.fill_(float(k))           # L2 flush between timed steps (not in the step time)
+            step(evs[k])
+        t_end.record(stream)
+        barrier()
+    t_apply = sum(e[0].elapsed_time(e[1]) for e in evs) * 1e-3 / args.steps
+    t_cheb = sum(e[2].elapsed_time(e[3]) for e in evs) * 1e-3 / args.steps
+    t_step = sum(e[0].elapsed_time(e[3]) - e[1].elapsed_time(e[2]) for e in evs) * 1e-3 / args.steps
+    t_apply, t_cheb, t_step = (max_over_ranks(t_apply), max_over_ranks(t_cheb), max_over_ranks(t_step))
+    value = world * N / t_apply / 1e9
+    roof = {"bound": "hbm", "achieved": alg["apply_bytes"] / t_apply / 1e9, "peak": hbm_peak, "unit": "GB/s",
+            "frac": alg["apply_bytes"] / t_apply / 1e9 / hbm_peak, "traffic": None,
+            "kernel": "sfmg_apply = k_init + k_apply<8,true> (CUDA events around the ABI call)",
+            "peak_kind": peak_kind, "algorithmic_bytes": alg["apply_bytes"]}
+
+    # ---------------- end to end through the host-buffer ABI (pinned host in, host out)
+    v_host = torch.empty(N, dtype=torch.float64).pin_memory()
+    un, vn = u_host.numpy(), v_host.numpy()
+    for _ in range(3):
+        lv.apply_host(un, vn)
+    barrier()
+    t0 = time.perf_counter()
+    e2e_steps = max(3, min(args.steps, 20))
+    for _ in range(e2e_steps):
+        lv.apply_host(un, vn)
+    t_e2e = max_over_ranks((time.perf_counter() - t0) / e2e_steps)
+    e2e = {"value": world * N / t_e2e / 1e9, "unit": UNIT, "h2d_bytes_per_step": 8 * N, "d2h_bytes_per_step": 8 * N,
+           "call": "sfmg_apply_host (pinned host u -> device -> A_D u -> host), wall clock per call (syncs)"}
+
+    extras = {}
+    if not args.quick:
+        extras = run_extras(args, sfmg, dev, stream, flush, hbm_peak)
+
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": "BASELINE config 2: 16^3 deformed hexes (x+0.1 sin sin sin), p=8, "
+                                  "mu=exp(3 sin2pix sin2piy sin2piz), N=129^3, u~U[-1,1] seed 1; step = A_D u + "
+                                  "one degree-4 Chebyshev-Jacobi application (b=0, x0=u)",
+                      "l2": "flushed between timed steps (512 MB write)", "parallelism": "replicas" if world > 1
+                      else "single GPU"},
+           "apply_ms": t_apply * 1e3, "cheb_step_ms": t_cheb / 4 * 1e3,
+           "cheb_step_gdofs": world * N / (t_cheb / 4) / 1e9,
+           "cheb_step_hbm_frac": alg["step_bytes"] / (t_cheb / 4) / 1e9 / hbm_peak,
+           "apply_tflops": alg["apply_flops"] / t_apply / 1e12,
+           "roofline": roof, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
+           "clocks": clk.summary()}
+    out.update(extras)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        gd, cores, sample = oracle_apply_sample(d, inputs.SEEDS[2])
+        out["cpu_baseline"] = {"value": gd, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+def time_events(fn, stream, flush, reps, warm=3):
+    import torch
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for k in range(reps):
+        flush.fill_(float(k))
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        fn()
+        b.record(stream)
+        b.synchronize()
+        ts.append(a.elapsed_time(b) * 1e-3)
+    return statistics.median(ts)
+
+
+def run_extras(args, sfmg, dev, stream, flush, hbm_peak):
+    import torch
+    out = {}
+    sweep = []
+    for p in (1, 2, 4, 8, 16):
+        d = inputs.CONFIG3[p]
+        alg = algorithmic(d)
+        lv = sfmg.Level(sfmg.Problem.from_dict(d), device=dev)
+        u = torch.from_numpy(inputs.uniform_pm1(inputs.SEEDS[3], lv.N)).to(dev)
+        v, b, x = torch.empty_like(u), torch.zeros_like(u), u.clone()
+        lam = lv.lambda_max(10, inputs.POWER_SEED)
+        ta = time_events(lambda: lv.apply(u, v), stream, flush, 20)
+        tc = time_events(lambda: lv.cheb(b, x, 4, 0.1 * lam, 1.1 * lam), stream, flush, 10) / 4
+        sweep.append({"p": p, "ne": d["nex"], "apply_us": ta * 1e6, "apply_gdofs": lv.N / ta / 1e9,
+                      "apply_hbm_frac": alg["apply_bytes"] / ta / 1e9 / hbm_peak,
+                      "apply_tflops": alg["apply_flops"] / ta / 1e12,
+                      "cheb_step_us": tc * 1e6, "cheb_step_gdofs": lv.N / tc / 1e9,
+                      "cheb_step_hbm_frac": alg["step_bytes"] / tc / 1e9 / hbm_peak})
+        del lv, u, v, b, x
+    out["sweep_config3"] = sweep
+    if not args.no_config4:
+        d = inputs.CONFIG4
+        alg = algorithmic(d)
+        lv = sfmg.Level(sfmg.Problem.from_dict(d), device=dev)
+        u = torch.from_numpy(inputs.uniform_pm1(inputs.SEEDS[4], lv.N)).to(dev)
+        v, b, x = torch.empty_like(u), torch.zeros_like(u), u.clone()
+        lam = lv.lambda_max(10, inputs.POWER_SEED)
+        ta = time_events(lambda: lv.apply(u, v), stream, flush, 10)
+        tc = time_events(lambda: lv.cheb(b, x, 4, 0.1 * lam, 1.1 * lam), stream, flush, 5) / 4
+        out["config4"] = {"N": lv.N, "apply_ms": ta * 1e3, "apply_gdofs": lv.N / ta / 1e9,
+                          "apply_hbm_frac": alg["apply_bytes"] / ta / 1e9 / hbm_peak,
+                          "cheb_step_ms": tc * 1e3, "cheb_step_gdofs": lv.N / tc / 1e9,
+                          "cheb_step_hbm_frac": alg["step_bytes"] / tc / 1e9 / hbm_peak}
+        del lv, u, v, b, x
+        torch.cuda.empty_cache()
+    # config 5: p-MG 16 -> 1, V(2,2) degree-4 Chebyshev, coarse CG 1e-10, PCG to 1e-8
+    d = inputs.CONFIG5
+    t0 = time.perf_counter()
+    H = sfmg.Hierarchy(sfmg.Problem.from_dict(d), sfmg.MgParams(), device=dev)
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t0
+    bvec = H.levels[0].load_vector(1)
+    H.solve(bvec, mode=1, rtol=1e-8)
+    torch.cuda.synchronize()
+    a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    xs, rep = H.solve(bvec, mode=1, rtol=1e-8)
+    e.record(stream)
+    e.synchronize()
+    t_solve = a.elapsed_time(e) * 1e-3
+    tv = time_events(lambda: H.vcycle(bvec, xs), stream, flush, 5, warm=1)
+    out["config5_pmg_pcg"] = {"N": H.N, "levels": H.nlevels, "setup_s": t_setup, "pcg_iterations": rep["iterations"],
+                              "converged": rep["converged"], "rel_residual": rep["r_norm"] / rep["r0_norm"],
+                              "solve_ms": t_solve * 1e3, "vcycle_ms": tv * 1e3, "fine_applies": rep["fine_applies"]}
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="sfmg", choices=["sfmg", "reference"])
+    ap.add_argument("--quick", action="store_true", help="main workload only (no sweep / config 4 / config 5)")
+    ap.add_argument("--no-config4", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    if world > 1:
+        import torch.distributed as dist
+        import torch
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_gpu(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -68,6 +68,7 @@ def lib():
         L.orc_assemble_dense.argtypes = [vp, i, vp]
         L.orc_apply.argtypes = [vp, i, vp, vp, i]
         L.orc_apply_elements.argtypes = [vp, vp, vp, i64, vp, i]
+        L.orc_level_cache_elements.argtypes = [vp, i64, vp]
         L.orc_apply_rows.argtypes = [vp, i, vp, i64, vp, vp, i]
         L.orc_diag.argtypes = [vp, i, vp]
         L.orc_lambda_max.argtypes = [vp, i, u64]
@@ -236,6 +237,10 @@ class Level:
         v = np.zeros(self.N)
         lib().orc_apply_elements(self.h, _p(u), _p(v), len(elems), _p(elems), tier)
         return v
+
+    def cache_elements(self, elems):
+        elems = np.ascontiguousarray(elems, dtype=np.int64)
+        lib().orc_level_cache_elements(self.h, len(elems), _p(elems))
 
     def apply_rows(self, u, rows, bc=0, tier=2):
         u = np.ascontiguousarray(u, dtype=np.float64)

