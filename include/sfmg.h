@@ -109,7 +109,9 @@ sfmg_status sfmg_level_info(sfmg_level lv, int64_t* n_dofs, int64_t* n_elem, int
 sfmg_status sfmg_export_l2g(sfmg_level lv, int32_t* d_l2g, void* stream);
 sfmg_status sfmg_export_mask(sfmg_level lv, uint8_t* d_mask, void* stream);
 sfmg_status sfmg_export_colors(sfmg_level lv, uint8_t* d_colors, void* stream);
-/* Geometric factors as stored, fp64 [E][6][(p+1)^3] with components (00,01,02,11,12,22). */
+/* Geometric factors as stored, fp64 [E][p+1][6][(p+1)^2]: element e, slice k (z index), component
+ * (00,01,02,11,12,22), point (i + (p+1) j).  Slice-major so that one element (and one k-slice) is
+ * one contiguous block for the TMA bulk copies of the apply kernel. */
 sfmg_status sfmg_export_geometry(sfmg_level lv, double* d_G, void* stream);
 
 /* ---------------------------------------------------------------- operator */

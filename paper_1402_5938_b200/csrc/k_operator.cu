@@ -41,6 +41,12 @@ cudaError_t upload_order_tables(int p, cudaStream_t s) {
 // ------------------------------------------------------------------------------------------
 // small device helpers
 
+// Layout of the geometric factors, slice-major per element: G[e][k][c][j][i], c in (00,01,02,11,
+// 12,22).  An element's factors are one contiguous 48 n^3-byte block (one TMA bulk copy), and a
+// k-slice of all six components is one contiguous 48 n^2-byte block.
+template <int N>
+__device__ __forceinline__ int gofs(int c, int ij, int k) { return k * 6 * N * N + c * N * N + ij; }
+
 __device__ __forceinline__ void elem_coords(const MeshDev& m, long long e, int& ex, int& ey, int& ez) {
   ex = (int)(e % m.nex);
   long long t = e / m.nex;
@@ -128,7 +134,7 @@ __device__ __forceinline__ void jacobian(const MeshDev& m, const double* sD, con
 }
 
 // ------------------------------------------------------------------------------------------
-// K1 geometric factors: one thread per (element, point), G [E][6][n^3].
+// K1 geometric factors: one thread per (element, point), G [E][k][6][n^2].
 
 template <int P>
 __global__ void __launch_bounds__(256) k_geometry(MeshDev m, double* __restrict__ G, int* bad) {
@@ -165,12 +171,12 @@ __global__ void __launch_bounds__(256) k_geometry(MeshDev m, double* __restrict_
     double X[3];
     node_pos<P>(m, sx, ex, ey, ez, i, j, k, X);
     double s = sw[i] * sw[j] * sw[k] * coeff_mu(m, X[0], X[1], X[2]) * det;
-    double* Ge = G + e * 6 * N3 + q;
+    double* Ge = G + e * 6 * N3 + gofs<N>(0, i + N * j, k);
     const int comp[6][2] = {{0, 0}, {0, 1}, {0, 2}, {1, 1}, {1, 2}, {2, 2}};
 #pragma unroll
     for (int c = 0; c < 6; ++c) {
       int a = comp[c][0], b = comp[c][1];
-      Ge[c * N3] = s * (Ji[a][0] * Ji[b][0] + Ji[a][1] * Ji[b][1] + Ji[a][2] * Ji[b][2]);
+      Ge[c * N2] = s * (Ji[a][0] * Ji[b][0] + Ji[a][1] * Ji[b][1] + Ji[a][2] * Ji[b][2]);
     }
   }
 }
@@ -275,12 +281,12 @@ __global__ void __launch_bounds__(ApplyCfg<P>::THREADS)
       const double g0 = s0[idx], g1 = s1[idx];
       double G00 = 0, G01 = 0, G02 = 0, G11 = 0, G12 = 0, G22 = 0;
       if (act) {
-        G00 = __ldcs(Ge + 0 * N3 + N2 * k);
-        G01 = __ldcs(Ge + 1 * N3 + N2 * k);
-        G02 = __ldcs(Ge + 2 * N3 + N2 * k);
-        G11 = __ldcs(Ge + 3 * N3 + N2 * k);
-        G12 = __ldcs(Ge + 4 * N3 + N2 * k);
-        G22 = __ldcs(Ge + 5 * N3 + N2 * k);
+        G00 = __ldcs(Ge + gofs<N>(0, 0, k));
+        G01 = __ldcs(Ge + gofs<N>(1, 0, k));
+        G02 = __ldcs(Ge + gofs<N>(2, 0, k));
+        G11 = __ldcs(Ge + gofs<N>(3, 0, k));
+        G12 = __ldcs(Ge + gofs<N>(4, 0, k));
+        G22 = __ldcs(Ge + gofs<N>(5, 0, k));
       }
       s0[idx] = G00 * g0 + G01 * g1 + G02 * g2;
       s1[idx] = G01 * g0 + G11 * g1 + G12 * g2;
@@ -333,6 +339,357 @@ __global__ void __launch_bounds__(ApplyCfg<P>::THREADS)
 }
 
 // ------------------------------------------------------------------------------------------
+// K2 apply, v2 (p <= 8): the block's geometric factors (EPB consecutive elements, one contiguous
+// block of 48 EPB n^3 bytes) are fetched into shared memory by ONE TMA bulk copy
+// (cp.async.bulk ... mbarrier::complete_tx) issued at block start, so the HBM stream overlaps the
+// gather and the first two derivative passes; blocks are small (<= ~50 KB smem) so 4 co-reside
+// per SM and keep >= 2 copies in flight.  Work arrays: 2 n^3 per element (line passes in place).
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+          smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+template <int P>
+struct V2Cfg {
+  static constexpr int N = P + 1, N2 = N * N, N3 = N2 * N;
+  static constexpr int EPB_SMEM = 50000 / (64 * N3) > 0 ? 50000 / (64 * N3) : 1;
+  static constexpr int EPB_THR = 256 / N2 > 0 ? 256 / N2 : 1;
+  static constexpr int EPB = EPB_SMEM < EPB_THR ? EPB_SMEM : EPB_THR;
+  static constexpr int THREADS = EPB * N2;
+  static constexpr size_t SMEM = (size_t)EPB * 8 * N3 * sizeof(double) + 16;
+  static constexpr int MINB = (227 * 1024) / (SMEM + 1024) < 8 ? (227 * 1024) / (SMEM + 1024) : 8;
+};
+
+template <int P, bool DIR>
+__global__ void __launch_bounds__(V2Cfg<P>::THREADS, V2Cfg<P>::MINB)
+    k_apply_v2(MeshDev m, const double* __restrict__ G, const double* __restrict__ u, double* __restrict__ v) {
+  using C = V2Cfg<P>;
+  constexpr int N = C::N, N2 = C::N2, N3 = C::N3;
+  extern __shared__ __align__(128) double smem[];
+  double* sG = smem;                                  // [EPB][k][6][n^2]
+  double* su = smem + C::EPB * 6 * N3;                // per element: su [n^3], s0 [n^3]
+  uint64_t* bar = (uint64_t*)(smem + C::EPB * 8 * N3);
+  const int le = threadIdx.x / N2;
+  const int t = threadIdx.x - le * N2;
+  const int t0 = t % N, t1 = t / N;
+  const long long e0 = (long long)blockIdx.x * C::EPB;
+  const long long e = e0 + le;
+  const bool act = e < m.E;
+  su += le * 2 * N3;
+  double* s0 = su + N3;
+  const double* gE = sG + le * 6 * N3;
+
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    long long nel = m.E - e0;
+    if (nel > C::EPB) nel = C::EPB;
+    bulk_load(sG, G + e0 * 6 * N3, (unsigned)(nel * 6 * N3 * sizeof(double)), bar);
+  }
+
+  int ex = 0, ey = 0, ez = 0;
+  if (act) elem_coords(m, e, ex, ey, ez);
+  const long long sxy = (long long)m.Mx * m.My;
+  const long long gcol = (long long)(ex * P + t0) + (long long)m.Mx * (ey * P + t1) + sxy * (long long)(ez * P);
+  bool bxy = false;
+  if (DIR) {
+    const int I = ex * P + t0, J = ey * P + t1;
+    bxy = (I == 0) || (I == m.Mx - 1) || (J == 0) || (J == m.My - 1);
+  }
+  double ru[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    double val = 0.0;
+    if (act) {
+      bool bnd = false;
+      if (DIR) { const int K = ez * P + k; bnd = bxy || K == 0 || K == m.Mz - 1; }
+      if (!bnd) val = __ldg(u + gcol + sxy * k);
+    }
+    ru[k] = val;
+    su[t0 + N * t1 + N2 * k] = val;
+  }
+  __syncthreads();
+  {  // P1: g0 on x-line (j=t0, k=t1) -> s0
+    double L[N];
+#pragma unroll
+    for (int mm = 0; mm < N; ++mm) L[mm] = su[mm + N * t0 + N2 * t1];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      double s = 0.0;
+#pragma unroll
+      for (int mm = 0; mm < N; ++mm) s = fma(c_D[P - 1][i * N + mm], L[mm], s);
+      s0[i + N * t0 + N2 * t1] = s;
+    }
+  }
+  __syncthreads();
+  {  // P2: g1 on y-line (i=t0, k=t1), in place in su
+    double L[N];
+#pragma unroll
+    for (int mm = 0; mm < N; ++mm) L[mm] = su[t0 + N * mm + N2 * t1];
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      double s = 0.0;
+#pragma unroll
+      for (int mm = 0; mm < N; ++mm) s = fma(c_D[P - 1][j * N + mm], L[mm], s);
+      su[t0 + N * j + N2 * t1] = s;
+    }
+  }
+  __syncthreads();
+  mbar_wait(bar, 0);
+  double vz[N];
+  {  // P3: g2 in registers, w = G g with G from shared memory, vz += D^T w2 accumulated per k
+#pragma unroll
+    for (int c = 0; c < N; ++c) vz[c] = 0.0;
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      double g2 = 0.0;
+#pragma unroll
+      for (int mm = 0; mm < N; ++mm) g2 = fma(c_D[P - 1][k * N + mm], ru[mm], g2);
+      const int idx = t + N2 * k;
+      const double g0 = s0[idx], g1 = su[idx];
+      const double* Gk = gE + gofs<N>(0, t, k);
+      const double G00 = Gk[0], G01 = Gk[N2], G02 = Gk[2 * N2], G11 = Gk[3 * N2], G12 = Gk[4 * N2], G22 = Gk[5 * N2];
+      s0[idx] = G00 * g0 + G01 * g1 + G02 * g2;
+      su[idx] = G01 * g0 + G11 * g1 + G12 * g2;
+      const double w2 = G02 * g0 + G12 * g1 + G22 * g2;
+#pragma unroll
+      for (int c = 0; c < N; ++c) vz[c] = fma(c_D[P - 1][k * N + c], w2, vz[c]);
+      if (N > 7) asm volatile("" ::: "memory");   // keep ptxas from hoisting every slice's loads
+    }
+  }
+  __syncthreads();
+  {  // P4: v0 = D^T w0 on x-line (j=t0, k=t1), in place in s0
+    double L[N];
+#pragma unroll
+    for (int mm = 0; mm < N; ++mm) L[mm] = s0[mm + N * t0 + N2 * t1];
+#pragma unroll
+    for (int a = 0; a < N; ++a) {
+      double s = 0.0;
+#pragma unroll
+      for (int mm = 0; mm < N; ++mm) s = fma(c_D[P - 1][mm * N + a], L[mm], s);
+      s0[a + N * t0 + N2 * t1] = s;
+    }
+  }
+  __syncthreads();
+  {  // P5: su = D^T w1 + v0 on y-line (i=t0, k=t1)
+    double L[N];
+#pragma unroll
+    for (int mm = 0; mm < N; ++mm) L[mm] = su[t0 + N * mm + N2 * t1];
+#pragma unroll
+    for (int b = 0; b < N; ++b) {
+      double s = s0[t0 + N * b + N2 * t1];
+#pragma unroll
+      for (int mm = 0; mm < N; ++mm) s = fma(c_D[P - 1][mm * N + b], L[mm], s);
+      su[t0 + N * b + N2 * t1] = s;
+    }
+  }
+  __syncthreads();
+  if (act) {  // P6: z-line (i=t0, j=t1): v = su + vz, scatter
+#pragma unroll
+    for (int c = 0; c < N; ++c) {
+      bool bnd = false;
+      if (DIR) { const int K = ez * P + c; bnd = bxy || K == 0 || K == m.Mz - 1; }
+      if (!bnd) atomicAdd(v + gcol + sxy * c, su[t + N2 * c] + vz[c]);
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// K2 apply, v3 (p <= 8): persistent version of v2.  Each block walks element groups
+// grp = blockIdx.x, blockIdx.x + gridDim.x, ...; as soon as P3 of group g has consumed the staged
+// factors, one thread issues (a) the TMA bulk copy of group g+1's factors into the same buffer and
+// (b) a TMA L2 prefetch (cp.async.bulk.prefetch.L2) of group g+2's factors, and every thread
+// prefetches its u column of group g+1 into L2.  HBM therefore always has the next-but-one
+// group of every resident block in flight, and the smem copy of the next group (from L2)
+// overlaps P4-P6 and the next gather/P1/P2.
+
+template <int P, bool DIR>
+__global__ void __launch_bounds__(V2Cfg<P>::THREADS, V2Cfg<P>::MINB)
+    k_apply_v3(MeshDev m, const double* __restrict__ G, const double* __restrict__ u, double* __restrict__ v,
+               long long ngroups) {
+  using C = V2Cfg<P>;
+  constexpr int N = C::N, N2 = C::N2, N3 = C::N3;
+  extern __shared__ __align__(128) double smem[];
+  double* sG = smem;
+  double* su = smem + C::EPB * 6 * N3;
+  uint64_t* bar = (uint64_t*)(smem + C::EPB * 8 * N3);
+  const int le = threadIdx.x / N2;
+  const int t = threadIdx.x - le * N2;
+  const int t0 = t % N, t1 = t / N;
+  su += le * 2 * N3;
+  double* s0 = su + N3;
+  const double* gE = sG + le * 6 * N3;
+  const long long sxy = (long long)m.Mx * m.My;
+  const long long gstride = gridDim.x;
+  auto group_bytes = [&](long long g) -> unsigned {
+    long long nel = m.E - g * C::EPB;
+    if (nel > C::EPB) nel = C::EPB;
+    return (unsigned)(nel * 6 * N3 * sizeof(double));
+  };
+
+  long long grp = blockIdx.x;
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    if (grp < ngroups) bulk_load(sG, G + grp * C::EPB * 6 * N3, group_bytes(grp), bar);
+    if (grp + gstride < ngroups) bulk_prefetch_l2(G + (grp + gstride) * C::EPB * 6 * N3, group_bytes(grp + gstride));
+  }
+  unsigned phase = 0;
+  for (; grp < ngroups; grp += gstride) {
+    const long long e = grp * C::EPB + le;
+    const bool act = e < m.E;
+    int ex = 0, ey = 0, ez = 0;
+    if (act) elem_coords(m, e, ex, ey, ez);
+    const long long gcol = (long long)(ex * P + t0) + (long long)m.Mx * (ey * P + t1) + sxy * (long long)(ez * P);
+    bool bxy = false;
+    if (DIR) {
+      const int I = ex * P + t0, J = ey * P + t1;
+      bxy = (I == 0) || (I == m.Mx - 1) || (J == 0) || (J == m.My - 1);
+    }
+    double ru[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      double val = 0.0;
+      if (act) {
+        bool bnd = false;
+        if (DIR) { const int K = ez * P + k; bnd = bxy || K == 0 || K == m.Mz - 1; }
+        if (!bnd) val = __ldg(u + gcol + sxy * k);
+      }
+      ru[k] = val;
+      su[t + N2 * k] = val;
+    }
+    __syncthreads();
+    {  // P1: g0 on x-line (j=t0, k=t1) -> s0
+      double L[N];
+#pragma unroll
+      for (int mm = 0; mm < N; ++mm) L[mm] = su[mm + N * t0 + N2 * t1];
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        double s = 0.0;
+#pragma unroll
+        for (int mm = 0; mm < N; ++mm) s = fma(c_D[P - 1][i * N + mm], L[mm], s);
+        s0[i + N * t0 + N2 * t1] = s;
+      }
+    }
+    __syncthreads();
+    {  // P2: g1 on y-line (i=t0, k=t1), in place in su
+      double L[N];
+#pragma unroll
+      for (int mm = 0; mm < N; ++mm) L[mm] = su[t0 + N * mm + N2 * t1];
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        double s = 0.0;
+#pragma unroll
+        for (int mm = 0; mm < N; ++mm) s = fma(c_D[P - 1][j * N + mm], L[mm], s);
+        su[t0 + N * j + N2 * t1] = s;
+      }
+    }
+    __syncthreads();
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    double vz[N];
+    {  // P3
+#pragma unroll
+      for (int c = 0; c < N; ++c) vz[c] = 0.0;
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        double g2 = 0.0;
+#pragma unroll
+        for (int mm = 0; mm < N; ++mm) g2 = fma(c_D[P - 1][k * N + mm], ru[mm], g2);
+        const int idx = t + N2 * k;
+        const double g0 = s0[idx], g1 = su[idx];
+        const double* Gk = gE + gofs<N>(0, t, k);
+        const double G00 = Gk[0], G01 = Gk[N2], G02 = Gk[2 * N2], G11 = Gk[3 * N2], G12 = Gk[4 * N2], G22 = Gk[5 * N2];
+        s0[idx] = G00 * g0 + G01 * g1 + G02 * g2;
+        su[idx] = G01 * g0 + G11 * g1 + G12 * g2;
+        const double w2 = G02 * g0 + G12 * g1 + G22 * g2;
+#pragma unroll
+        for (int c = 0; c < N; ++c) vz[c] = fma(c_D[P - 1][k * N + c], w2, vz[c]);
+      }
+    }
+    __syncthreads();
+    {  // staged factors consumed: start the next group's copy (from L2) and the one after's L2 prefetch
+      const long long nx = grp + gstride;
+      if (nx < ngroups) {
+        if (threadIdx.x == 0) {
+          fence_proxy_async_smem();
+          bulk_load(sG, G + nx * C::EPB * 6 * N3, group_bytes(nx), bar);
+          if (nx + gstride < ngroups)
+            bulk_prefetch_l2(G + (nx + gstride) * C::EPB * 6 * N3, group_bytes(nx + gstride));
+        }
+        const long long en = nx * C::EPB + le;
+        if (en < m.E) {
+          int fx, fy, fz;
+          elem_coords(m, en, fx, fy, fz);
+          const double* pu = u + (long long)(fx * P + t0) + (long long)m.Mx * (fy * P + t1) + sxy * (long long)(fz * P);
+#pragma unroll
+          for (int k = 0; k < N; ++k) asm volatile("prefetch.global.L2 [%0];" ::"l"(pu + sxy * k));
+        }
+      }
+    }
+    {  // P4: v0 = D^T w0 on x-line (j=t0, k=t1), in place in s0
+      double L[N];
+#pragma unroll
+      for (int mm = 0; mm < N; ++mm) L[mm] = s0[mm + N * t0 + N2 * t1];
+#pragma unroll
+      for (int a = 0; a < N; ++a) {
+        double s = 0.0;
+#pragma unroll
+        for (int mm = 0; mm < N; ++mm) s = fma(c_D[P - 1][mm * N + a], L[mm], s);
+        s0[a + N * t0 + N2 * t1] = s;
+      }
+    }
+    __syncthreads();
+    {  // P5: su = D^T w1 + v0 on y-line (i=t0, k=t1)
+      double L[N];
+#pragma unroll
+      for (int mm = 0; mm < N; ++mm) L[mm] = su[t0 + N * mm + N2 * t1];
+#pragma unroll
+      for (int b = 0; b < N; ++b) {
+        double s = s0[t0 + N * b + N2 * t1];
+#pragma unroll
+        for (int mm = 0; mm < N; ++mm) s = fma(c_D[P - 1][mm * N + b], L[mm], s);
+        su[t0 + N * b + N2 * t1] = s;
+      }
+    }
+    __syncthreads();
+    if (act) {  // P6: z-line (i=t0, j=t1): v = su + vz, scatter (su column is this thread's own)
+#pragma unroll
+      for (int c = 0; c < N; ++c) {
+        bool bnd = false;
+        if (DIR) { const int K = ez * P + c; bnd = bxy || K == 0 || K == m.Mz - 1; }
+        if (!bnd) atomicAdd(v + gcol + sxy * c, su[t + N2 * c] + vz[c]);
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
 // K3 diagonal: for node (a,b,c) of element e
 //   sum_i D[i][a]^2 G00(i,b,c) + sum_j D[j][b]^2 G11(a,j,c) + sum_k D[k][c]^2 G22(a,b,k)
 //   + 2 D[a][a] D[b][b] G01(a,b,c) + 2 D[a][a] D[c][c] G02(a,b,c) + 2 D[b][b] D[c][c] G12(a,b,c)
@@ -355,11 +712,13 @@ __global__ void __launch_bounds__(256) k_diag(MeshDev m, int bc, const double* _
     if (bc == 0 && lattice_boundary(m, g)) continue;
     const double* Ge = G + e * 6 * N3;
     double s = 0.0;
-    for (int i = 0; i < N; ++i) s += sD[i * N + a] * sD[i * N + a] * Ge[0 * N3 + i + N * b + N2 * c];
-    for (int j = 0; j < N; ++j) s += sD[j * N + b] * sD[j * N + b] * Ge[3 * N3 + a + N * j + N2 * c];
-    for (int k = 0; k < N; ++k) s += sD[k * N + c] * sD[k * N + c] * Ge[5 * N3 + a + N * b + N2 * k];
+    for (int i = 0; i < N; ++i) s += sD[i * N + a] * sD[i * N + a] * Ge[gofs<N>(0, i + N * b, c)];
+    for (int j = 0; j < N; ++j) s += sD[j * N + b] * sD[j * N + b] * Ge[gofs<N>(3, a + N * j, c)];
+    for (int k = 0; k < N; ++k) s += sD[k * N + c] * sD[k * N + c] * Ge[gofs<N>(5, a + N * b, k)];
     const double da = sD[a * N + a], db = sD[b * N + b], dc = sD[c * N + c];
-    s += 2.0 * da * db * Ge[1 * N3 + l] + 2.0 * da * dc * Ge[2 * N3 + l] + 2.0 * db * dc * Ge[4 * N3 + l];
+    const int ab = a + N * b;
+    s += 2.0 * da * db * Ge[gofs<N>(1, ab, c)] + 2.0 * da * dc * Ge[gofs<N>(2, ab, c)] +
+         2.0 * db * dc * Ge[gofs<N>(4, ab, c)];
     atomicAdd(d + g, s);
   }
 }
@@ -498,7 +857,6 @@ __device__ void cta_apply(const MeshDev& m, const double* __restrict__ G, const 
       for (int j = 0; j < N; ++j)
 #pragma unroll
         for (int i = 0; i < N; ++i) {
-          const int q = i + N * (j + N * k);
           double g0 = 0, g1 = 0, g2 = 0;
 #pragma unroll
           for (int mm = 0; mm < N; ++mm) {
@@ -506,8 +864,9 @@ __device__ void cta_apply(const MeshDev& m, const double* __restrict__ G, const 
             g1 = fma(c_D[P - 1][j * N + mm], ue[i + N * (mm + N * k)], g1);
             g2 = fma(c_D[P - 1][k * N + mm], ue[i + N * (j + N * mm)], g2);
           }
-          const double G00 = Ge[q], G01 = Ge[N3 + q], G02 = Ge[2 * N3 + q];
-          const double G11 = Ge[3 * N3 + q], G12 = Ge[4 * N3 + q], G22 = Ge[5 * N3 + q];
+          const int ij = i + N * j;
+          const double G00 = Ge[gofs<N>(0, ij, k)], G01 = Ge[gofs<N>(1, ij, k)], G02 = Ge[gofs<N>(2, ij, k)];
+          const double G11 = Ge[gofs<N>(3, ij, k)], G12 = Ge[gofs<N>(4, ij, k)], G22 = Ge[gofs<N>(5, ij, k)];
           const double w0 = G00 * g0 + G01 * g1 + G02 * g2;
           const double w1 = G01 * g0 + G11 * g1 + G12 * g2;
           const double w2 = G02 * g0 + G12 * g1 + G22 * g2;
@@ -612,6 +971,26 @@ cudaError_t launch_geometry(const MeshDev& m, double* G, int* bad, cudaStream_t 
 
 template <int P, bool DIR>
 static cudaError_t apply_pd(const MeshDev& m, const double* G, const double* u, double* v, cudaStream_t s) {
+  if constexpr (P <= 8) {
+    using C = V2Cfg<P>;
+    static int resident = 0;   // blocks per SM of the persistent kernel
+    static int num_sms = 0;
+    if (!resident) {
+      cudaError_t e = cudaFuncSetAttribute(k_apply_v3<P, DIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+      if (e) return e;
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_apply_v3<P, DIR>, C::THREADS, C::SMEM);
+      if (e) return e;
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+      if (resident < 1) resident = 1;
+    }
+    const long long groups = (m.E + C::EPB - 1) / C::EPB;
+    long long grid = (long long)resident * num_sms;
+    if (grid > groups) grid = groups;
+    k_apply_v3<P, DIR><<<(unsigned)grid, C::THREADS, C::SMEM, s>>>(m, G, u, v, groups);
+    return cudaSuccess;
+  }
   using C = ApplyCfg<P>;
   static bool attr = false;
   if (!attr) {

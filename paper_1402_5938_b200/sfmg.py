@@ -232,7 +232,7 @@ class Level:
         return a
 
     def export_geometry(self, stream=None):
-        a = torch.empty((self.E, 6, self.n ** 3), dtype=torch.float64, device=self.device)
+        a = torch.empty((self.E, self.n, 6, self.n ** 2), dtype=torch.float64, device=self.device)
         _ck(_lib.sfmg_export_geometry(self.h, _dptr(a), _stream(stream)), "sfmg_export_geometry")
         return a
 

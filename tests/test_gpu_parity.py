@@ -68,7 +68,9 @@ def test_index_maps_bit_exact(S, orc, d):
 def test_geometry_apply_diag_small(S, orc, d):
     g = gpu_level(S, d)
     o = orc_level(orc, d)
-    G = g.export_geometry().cpu().numpy()
+    n = d["p"] + 1
+    # exported layout [E][k][6][n^2] -> oracle's [6][n^3] with q = (i + n j) + n^2 k
+    G = g.export_geometry().cpu().numpy().reshape(o.E, n, 6, n * n).transpose(0, 2, 1, 3).reshape(o.E, 6, n ** 3)
     for e in range(o.E):
         Go, _, _ = o.geometry(e)
         assert rel_err(G[e], Go, np.abs(Go).max()) <= 1e-12
