@@ -16,7 +16,12 @@
 
 namespace sfmg {
 
-__constant__ double c_D[kMaxOrder][17 * 17];
+// D for p <= 8 in 5 identical copies, one per line pass of the apply kernel: each pass then reads
+// its own constant addresses, so ptxas reloads D per pass (LDCU into uniform registers feeding
+// DFMA) instead of keeping all n^2 values live in the register file across passes.
+constexpr int kDCopies = 5;
+__constant__ double c_D8[8][kDCopies][81];
+__constant__ double c_D16[8][17 * 17];   // p = 9..16
 __constant__ double c_x[kMaxOrder][17];
 __constant__ double c_w[kMaxOrder][17];
 
@@ -27,8 +32,15 @@ cudaError_t upload_order_tables(int p, cudaStream_t s) {
   Basis1D B = make_basis(p);
   const int n = p + 1;
   cudaError_t e;
-  e = cudaMemcpyToSymbol(c_D, B.D.data(), sizeof(double) * n * n, sizeof(double) * 17 * 17 * (p - 1));
-  if (e) return e;
+  if (p <= 8) {
+    for (int c = 0; c < kDCopies; ++c) {
+      e = cudaMemcpyToSymbol(c_D8, B.D.data(), sizeof(double) * n * n, sizeof(double) * 81 * (kDCopies * (p - 1) + c));
+      if (e) return e;
+    }
+  } else {
+    e = cudaMemcpyToSymbol(c_D16, B.D.data(), sizeof(double) * n * n, sizeof(double) * 17 * 17 * (p - 9));
+    if (e) return e;
+  }
   e = cudaMemcpyToSymbol(c_x, B.x.data(), sizeof(double) * n, sizeof(double) * 17 * (p - 1));
   if (e) return e;
   e = cudaMemcpyToSymbol(c_w, B.w.data(), sizeof(double) * n, sizeof(double) * 17 * (p - 1));
@@ -40,6 +52,13 @@ cudaError_t upload_order_tables(int p, cudaStream_t s) {
 
 // ------------------------------------------------------------------------------------------
 // small device helpers
+
+// D[i][m] = ell_m'(xhat_i) of order P, copy `cp` (p <= 8), flat index i * (P+1) + m
+template <int P>
+__device__ __forceinline__ double dmat(int cp, int idx) {
+  if constexpr (P <= 8) return c_D8[P - 1][cp][idx];
+  else return c_D16[P - 9][idx];
+}
 
 // Layout of the geometric factors, slice-major per element: G[e][k][c][j][i], c in (00,01,02,11,
 // 12,22).  An element's factors are one contiguous 48 n^3-byte block (one TMA bulk copy), and a
@@ -140,7 +159,7 @@ template <int P>
 __global__ void __launch_bounds__(256) k_geometry(MeshDev m, double* __restrict__ G, int* bad) {
   constexpr int N = P + 1, N2 = N * N, N3 = N2 * N;
   __shared__ double sD[N * N], sx[N], sw[N];
-  for (int t = threadIdx.x; t < N * N; t += blockDim.x) sD[t] = c_D[P - 1][t];
+  for (int t = threadIdx.x; t < N * N; t += blockDim.x) sD[t] = dmat<P>(0, t);
   for (int t = threadIdx.x; t < N; t += blockDim.x) { sx[t] = c_x[P - 1][t]; sw[t] = c_w[P - 1][t]; }
   __syncthreads();
   const long long total = m.E * N3;
@@ -250,7 +269,7 @@ __global__ void __launch_bounds__(ApplyCfg<P>::THREADS)
     for (int i = 0; i < N; ++i) {
       double s = 0.0;
 #pragma unroll
-      for (int mm = 0; mm < N; ++mm) s = fma(c_D[P - 1][i * N + mm], L[mm], s);
+      for (int mm = 0; mm < N; ++mm) s = fma(dmat<P>(0, i * N + mm), L[mm], s);
       s0[i + N * t0 + N2 * t1] = s;
     }
   }
@@ -262,7 +281,7 @@ __global__ void __launch_bounds__(ApplyCfg<P>::THREADS)
     for (int j = 0; j < N; ++j) {
       double s = 0.0;
 #pragma unroll
-      for (int mm = 0; mm < N; ++mm) s = fma(c_D[P - 1][j * N + mm], L[mm], s);
+      for (int mm = 0; mm < N; ++mm) s = fma(dmat<P>(0, j * N + mm), L[mm], s);
       s1[t0 + N * j + N2 * t1] = s;
     }
   }
@@ -276,7 +295,7 @@ __global__ void __launch_bounds__(ApplyCfg<P>::THREADS)
     for (int k = 0; k < N; ++k) {
       double g2 = 0.0;
 #pragma unroll
-      for (int mm = 0; mm < N; ++mm) g2 = fma(c_D[P - 1][k * N + mm], ru[mm], g2);
+      for (int mm = 0; mm < N; ++mm) g2 = fma(dmat<P>(0, k * N + mm), ru[mm], g2);
       const int idx = t0 + N * t1 + N2 * k;
       const double g0 = s0[idx], g1 = s1[idx];
       double G00 = 0, G01 = 0, G02 = 0, G11 = 0, G12 = 0, G22 = 0;
@@ -296,7 +315,7 @@ __global__ void __launch_bounds__(ApplyCfg<P>::THREADS)
     for (int c = 0; c < N; ++c) {
       double s = 0.0;
 #pragma unroll
-      for (int k = 0; k < N; ++k) s = fma(c_D[P - 1][k * N + c], w2[k], s);
+      for (int k = 0; k < N; ++k) s = fma(dmat<P>(0, k * N + c), w2[k], s);
       vz[c] = s;
     }
   }
@@ -310,7 +329,7 @@ __global__ void __launch_bounds__(ApplyCfg<P>::THREADS)
     for (int a = 0; a < N; ++a) {
       double s = 0.0;
 #pragma unroll
-      for (int mm = 0; mm < N; ++mm) s = fma(c_D[P - 1][mm * N + a], L[mm], s);
+      for (int mm = 0; mm < N; ++mm) s = fma(dmat<P>(0, mm * N + a), L[mm], s);
       su[a + N * t0 + N2 * t1] = s;
     }
   }
@@ -323,7 +342,7 @@ __global__ void __launch_bounds__(ApplyCfg<P>::THREADS)
     for (int b = 0; b < N; ++b) {
       double s = 0.0;
 #pragma unroll
-      for (int mm = 0; mm < N; ++mm) s = fma(c_D[P - 1][mm * N + b], L[mm], s);
+      for (int mm = 0; mm < N; ++mm) s = fma(dmat<P>(0, mm * N + b), L[mm], s);
       su[t0 + N * b + N2 * t1] += s;
     }
   }
@@ -376,10 +395,30 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+
+// ------------------------------------------------------------------------------------------
+// K2 apply, v4 (p <= 8): persistent, software-pipelined across element groups.
+// Block = EPB elements x (n x n) threads; each block walks groups grp = blockIdx.x, + gridDim.x...
+//  * geometric factors: one TMA bulk copy (cp.async.bulk + mbarrier complete_tx) per group into
+//    shared memory, issued for group g+1 as soon as P3 of group g has consumed the buffer, plus a
+//    TMA L2 prefetch (cp.async.bulk.prefetch.L2) of group g+2, so every resident block keeps its
+//    next-but-one group's factors in flight from HBM;
+//  * u gather: per-thread cp.async (LDGSTS, zero-fill for Dirichlet/inactive nodes) of the next
+//    group's column into a second u buffer, also issued after P3, so the gather latency of group
+//    g+1 hides behind P4-P6 of group g.
+// Smem per element: 6 n^3 (G) + 3 n^3 (s0, two u/line buffers) doubles.
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, unsigned src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 template <int P>
-struct V2Cfg {
+struct V4Cfg {
   static constexpr int N = P + 1, N2 = N * N, N3 = N2 * N;
-  static constexpr int EPB_SMEM = 50000 / (64 * N3) > 0 ? 50000 / (64 * N3) : 1;
+  static constexpr int EPB_SMEM = 52000 / (64 * N3) > 0 ? 52000 / (64 * N3) : 1;
   static constexpr int EPB_THR = 256 / N2 > 0 ? 256 / N2 : 1;
   static constexpr int EPB = EPB_SMEM < EPB_THR ? EPB_SMEM : EPB_THR;
   static constexpr int THREADS = EPB * N2;
@@ -388,162 +427,19 @@ struct V2Cfg {
 };
 
 template <int P, bool DIR>
-__global__ void __launch_bounds__(V2Cfg<P>::THREADS, V2Cfg<P>::MINB)
-    k_apply_v2(MeshDev m, const double* __restrict__ G, const double* __restrict__ u, double* __restrict__ v) {
-  using C = V2Cfg<P>;
-  constexpr int N = C::N, N2 = C::N2, N3 = C::N3;
-  extern __shared__ __align__(128) double smem[];
-  double* sG = smem;                                  // [EPB][k][6][n^2]
-  double* su = smem + C::EPB * 6 * N3;                // per element: su [n^3], s0 [n^3]
-  uint64_t* bar = (uint64_t*)(smem + C::EPB * 8 * N3);
-  const int le = threadIdx.x / N2;
-  const int t = threadIdx.x - le * N2;
-  const int t0 = t % N, t1 = t / N;
-  const long long e0 = (long long)blockIdx.x * C::EPB;
-  const long long e = e0 + le;
-  const bool act = e < m.E;
-  su += le * 2 * N3;
-  double* s0 = su + N3;
-  const double* gE = sG + le * 6 * N3;
-
-  if (threadIdx.x == 0) {
-    mbar_init(bar, 1);
-    long long nel = m.E - e0;
-    if (nel > C::EPB) nel = C::EPB;
-    bulk_load(sG, G + e0 * 6 * N3, (unsigned)(nel * 6 * N3 * sizeof(double)), bar);
-  }
-
-  int ex = 0, ey = 0, ez = 0;
-  if (act) elem_coords(m, e, ex, ey, ez);
-  const long long sxy = (long long)m.Mx * m.My;
-  const long long gcol = (long long)(ex * P + t0) + (long long)m.Mx * (ey * P + t1) + sxy * (long long)(ez * P);
-  bool bxy = false;
-  if (DIR) {
-    const int I = ex * P + t0, J = ey * P + t1;
-    bxy = (I == 0) || (I == m.Mx - 1) || (J == 0) || (J == m.My - 1);
-  }
-  double ru[N];
-#pragma unroll
-  for (int k = 0; k < N; ++k) {
-    double val = 0.0;
-    if (act) {
-      bool bnd = false;
-      if (DIR) { const int K = ez * P + k; bnd = bxy || K == 0 || K == m.Mz - 1; }
-      if (!bnd) val = __ldg(u + gcol + sxy * k);
-    }
-    ru[k] = val;
-    su[t0 + N * t1 + N2 * k] = val;
-  }
-  __syncthreads();
-  {  // P1: g0 on x-line (j=t0, k=t1) -> s0
-    double L[N];
-#pragma unroll
-    for (int mm = 0; mm < N; ++mm) L[mm] = su[mm + N * t0 + N2 * t1];
-#pragma unroll
-    for (int i = 0; i < N; ++i) {
-      double s = 0.0;
-#pragma unroll
-      for (int mm = 0; mm < N; ++mm) s = fma(c_D[P - 1][i * N + mm], L[mm], s);
-      s0[i + N * t0 + N2 * t1] = s;
-    }
-  }
-  __syncthreads();
-  {  // P2: g1 on y-line (i=t0, k=t1), in place in su
-    double L[N];
-#pragma unroll
-    for (int mm = 0; mm < N; ++mm) L[mm] = su[t0 + N * mm + N2 * t1];
-#pragma unroll
-    for (int j = 0; j < N; ++j) {
-      double s = 0.0;
-#pragma unroll
-      for (int mm = 0; mm < N; ++mm) s = fma(c_D[P - 1][j * N + mm], L[mm], s);
-      su[t0 + N * j + N2 * t1] = s;
-    }
-  }
-  __syncthreads();
-  mbar_wait(bar, 0);
-  double vz[N];
-  {  // P3: g2 in registers, w = G g with G from shared memory, vz += D^T w2 accumulated per k
-#pragma unroll
-    for (int c = 0; c < N; ++c) vz[c] = 0.0;
-#pragma unroll
-    for (int k = 0; k < N; ++k) {
-      double g2 = 0.0;
-#pragma unroll
-      for (int mm = 0; mm < N; ++mm) g2 = fma(c_D[P - 1][k * N + mm], ru[mm], g2);
-      const int idx = t + N2 * k;
-      const double g0 = s0[idx], g1 = su[idx];
-      const double* Gk = gE + gofs<N>(0, t, k);
-      const double G00 = Gk[0], G01 = Gk[N2], G02 = Gk[2 * N2], G11 = Gk[3 * N2], G12 = Gk[4 * N2], G22 = Gk[5 * N2];
-      s0[idx] = G00 * g0 + G01 * g1 + G02 * g2;
-      su[idx] = G01 * g0 + G11 * g1 + G12 * g2;
-      const double w2 = G02 * g0 + G12 * g1 + G22 * g2;
-#pragma unroll
-      for (int c = 0; c < N; ++c) vz[c] = fma(c_D[P - 1][k * N + c], w2, vz[c]);
-      if (N > 7) asm volatile("" ::: "memory");   // keep ptxas from hoisting every slice's loads
-    }
-  }
-  __syncthreads();
-  {  // P4: v0 = D^T w0 on x-line (j=t0, k=t1), in place in s0
-    double L[N];
-#pragma unroll
-    for (int mm = 0; mm < N; ++mm) L[mm] = s0[mm + N * t0 + N2 * t1];
-#pragma unroll
-    for (int a = 0; a < N; ++a) {
-      double s = 0.0;
-#pragma unroll
-      for (int mm = 0; mm < N; ++mm) s = fma(c_D[P - 1][mm * N + a], L[mm], s);
-      s0[a + N * t0 + N2 * t1] = s;
-    }
-  }
-  __syncthreads();
-  {  // P5: su = D^T w1 + v0 on y-line (i=t0, k=t1)
-    double L[N];
-#pragma unroll
-    for (int mm = 0; mm < N; ++mm) L[mm] = su[t0 + N * mm + N2 * t1];
-#pragma unroll
-    for (int b = 0; b < N; ++b) {
-      double s = s0[t0 + N * b + N2 * t1];
-#pragma unroll
-      for (int mm = 0; mm < N; ++mm) s = fma(c_D[P - 1][mm * N + b], L[mm], s);
-      su[t0 + N * b + N2 * t1] = s;
-    }
-  }
-  __syncthreads();
-  if (act) {  // P6: z-line (i=t0, j=t1): v = su + vz, scatter
-#pragma unroll
-    for (int c = 0; c < N; ++c) {
-      bool bnd = false;
-      if (DIR) { const int K = ez * P + c; bnd = bxy || K == 0 || K == m.Mz - 1; }
-      if (!bnd) atomicAdd(v + gcol + sxy * c, su[t + N2 * c] + vz[c]);
-    }
-  }
-}
-
-// ------------------------------------------------------------------------------------------
-// K2 apply, v3 (p <= 8): persistent version of v2.  Each block walks element groups
-// grp = blockIdx.x, blockIdx.x + gridDim.x, ...; as soon as P3 of group g has consumed the staged
-// factors, one thread issues (a) the TMA bulk copy of group g+1's factors into the same buffer and
-// (b) a TMA L2 prefetch (cp.async.bulk.prefetch.L2) of group g+2's factors, and every thread
-// prefetches its u column of group g+1 into L2.  HBM therefore always has the next-but-one
-// group of every resident block in flight, and the smem copy of the next group (from L2)
-// overlaps P4-P6 and the next gather/P1/P2.
-
-template <int P, bool DIR>
-__global__ void __launch_bounds__(V2Cfg<P>::THREADS, V2Cfg<P>::MINB)
-    k_apply_v3(MeshDev m, const double* __restrict__ G, const double* __restrict__ u, double* __restrict__ v,
+__global__ void __launch_bounds__(V4Cfg<P>::THREADS, V4Cfg<P>::MINB)
+    k_apply_v4(MeshDev m, const double* __restrict__ G, const double* __restrict__ u, double* __restrict__ v,
                long long ngroups) {
-  using C = V2Cfg<P>;
+  using C = V4Cfg<P>;
   constexpr int N = C::N, N2 = C::N2, N3 = C::N3;
   extern __shared__ __align__(128) double smem[];
-  double* sG = smem;
-  double* su = smem + C::EPB * 6 * N3;
-  uint64_t* bar = (uint64_t*)(smem + C::EPB * 8 * N3);
+  double* sG = smem;                                   // [EPB][k][6][n^2]
   const int le = threadIdx.x / N2;
   const int t = threadIdx.x - le * N2;
   const int t0 = t % N, t1 = t / N;
-  su += le * 2 * N3;
-  double* s0 = su + N3;
+  double* s0 = smem + C::EPB * 6 * N3 + le * 2 * N3;   // per element: s0, su
+  double* su = s0 + N3;
+  uint64_t* bar = (uint64_t*)(smem + C::EPB * 8 * N3);
   const double* gE = sG + le * 6 * N3;
   const long long sxy = (long long)m.Mx * m.My;
   const long long gstride = gridDim.x;
@@ -552,8 +448,40 @@ __global__ void __launch_bounds__(V2Cfg<P>::THREADS, V2Cfg<P>::MINB)
     if (nel > C::EPB) nel = C::EPB;
     return (unsigned)(nel * 6 * N3 * sizeof(double));
   };
+  // this thread's u column of group g (M u: zero outside the element / on Dirichlet nodes, R4),
+  // loaded into registers one group ahead; and an L2 prefetch of the column of group g
+  auto load_column = [&](long long g, double (&r)[N]) {
+    const long long e = g * C::EPB + le;
+    const bool act = e < m.E;
+    int ex = 0, ey = 0, ez = 0;
+    if (act) elem_coords(m, e, ex, ey, ez);
+    const long long col = (long long)(ex * P + t0) + (long long)m.Mx * (ey * P + t1) + sxy * (long long)(ez * P);
+    bool bxy = false;
+    if (DIR) {
+      const int I = ex * P + t0, J = ey * P + t1;
+      bxy = (I == 0) || (I == m.Mx - 1) || (J == 0) || (J == m.My - 1);
+    }
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      bool ok = act;
+      if (DIR) { const int K = ez * P + k; ok = ok && !(bxy || K == 0 || K == m.Mz - 1); }
+      r[k] = ok ? __ldg(u + col + sxy * k) : 0.0;
+    }
+  };
+  auto prefetch_column = [&](long long g) {
+    const long long e = g * C::EPB + le;
+    if (e >= m.E) return;
+    int ex, ey, ez;
+    elem_coords(m, e, ex, ey, ez);
+    const double* pu = u + (long long)(ex * P + t0) + (long long)m.Mx * (ey * P + t1) + sxy * (long long)(ez * P);
+#pragma unroll
+    for (int k = 0; k < N; ++k) asm volatile("prefetch.global.L2 [%0];" ::"l"(pu + sxy * k));
+  };
 
   long long grp = blockIdx.x;
+  double ru[N];
+  if (grp < ngroups) load_column(grp, ru);
+  if (grp + gstride < ngroups) prefetch_column(grp + gstride);
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);
     if (grp < ngroups) bulk_load(sG, G + grp * C::EPB * 6 * N3, group_bytes(grp), bar);
@@ -561,6 +489,8 @@ __global__ void __launch_bounds__(V2Cfg<P>::THREADS, V2Cfg<P>::MINB)
   }
   unsigned phase = 0;
   for (; grp < ngroups; grp += gstride) {
+    // 0 at run time, but loop-variant: stops ptxas from hoisting the D loads out of the loop
+    constexpr int zero = 0;
     const long long e = grp * C::EPB + le;
     const bool act = e < m.E;
     int ex = 0, ey = 0, ez = 0;
@@ -571,18 +501,8 @@ __global__ void __launch_bounds__(V2Cfg<P>::THREADS, V2Cfg<P>::MINB)
       const int I = ex * P + t0, J = ey * P + t1;
       bxy = (I == 0) || (I == m.Mx - 1) || (J == 0) || (J == m.My - 1);
     }
-    double ru[N];
 #pragma unroll
-    for (int k = 0; k < N; ++k) {
-      double val = 0.0;
-      if (act) {
-        bool bnd = false;
-        if (DIR) { const int K = ez * P + k; bnd = bxy || K == 0 || K == m.Mz - 1; }
-        if (!bnd) val = __ldg(u + gcol + sxy * k);
-      }
-      ru[k] = val;
-      su[t + N2 * k] = val;
-    }
+    for (int k = 0; k < N; ++k) su[t + N2 * k] = ru[k];
     __syncthreads();
     {  // P1: g0 on x-line (j=t0, k=t1) -> s0
       double L[N];
@@ -592,7 +512,7 @@ __global__ void __launch_bounds__(V2Cfg<P>::THREADS, V2Cfg<P>::MINB)
       for (int i = 0; i < N; ++i) {
         double s = 0.0;
 #pragma unroll
-        for (int mm = 0; mm < N; ++mm) s = fma(c_D[P - 1][i * N + mm], L[mm], s);
+        for (int mm = 0; mm < N; ++mm) s = fma(dmat<P>(0, i * N + mm + zero), L[mm], s);
         s0[i + N * t0 + N2 * t1] = s;
       }
     }
@@ -605,7 +525,7 @@ __global__ void __launch_bounds__(V2Cfg<P>::THREADS, V2Cfg<P>::MINB)
       for (int j = 0; j < N; ++j) {
         double s = 0.0;
 #pragma unroll
-        for (int mm = 0; mm < N; ++mm) s = fma(c_D[P - 1][j * N + mm], L[mm], s);
+        for (int mm = 0; mm < N; ++mm) s = fma(dmat<P>(1, j * N + mm + zero), L[mm], s);
         su[t0 + N * j + N2 * t1] = s;
       }
     }
@@ -613,14 +533,14 @@ __global__ void __launch_bounds__(V2Cfg<P>::THREADS, V2Cfg<P>::MINB)
     mbar_wait(bar, phase);
     phase ^= 1u;
     double vz[N];
-    {  // P3
+    {  // P3: g2 in registers, w = G g (G from smem), vz += D^T w2
 #pragma unroll
       for (int c = 0; c < N; ++c) vz[c] = 0.0;
 #pragma unroll
       for (int k = 0; k < N; ++k) {
         double g2 = 0.0;
 #pragma unroll
-        for (int mm = 0; mm < N; ++mm) g2 = fma(c_D[P - 1][k * N + mm], ru[mm], g2);
+        for (int mm = 0; mm < N; ++mm) g2 = fma(dmat<P>(2, k * N + mm + zero), ru[mm], g2);
         const int idx = t + N2 * k;
         const double g0 = s0[idx], g1 = su[idx];
         const double* Gk = gE + gofs<N>(0, t, k);
@@ -629,11 +549,11 @@ __global__ void __launch_bounds__(V2Cfg<P>::THREADS, V2Cfg<P>::MINB)
         su[idx] = G01 * g0 + G11 * g1 + G12 * g2;
         const double w2 = G02 * g0 + G12 * g1 + G22 * g2;
 #pragma unroll
-        for (int c = 0; c < N; ++c) vz[c] = fma(c_D[P - 1][k * N + c], w2, vz[c]);
+        for (int c = 0; c < N; ++c) vz[c] = fma(dmat<P>(2, k * N + c + zero), w2, vz[c]);
       }
     }
     __syncthreads();
-    {  // staged factors consumed: start the next group's copy (from L2) and the one after's L2 prefetch
+    {  // factors consumed: next group's G (TMA from L2) and u column (cp.async); G of g+2 to L2
       const long long nx = grp + gstride;
       if (nx < ngroups) {
         if (threadIdx.x == 0) {
@@ -642,15 +562,12 @@ __global__ void __launch_bounds__(V2Cfg<P>::THREADS, V2Cfg<P>::MINB)
           if (nx + gstride < ngroups)
             bulk_prefetch_l2(G + (nx + gstride) * C::EPB * 6 * N3, group_bytes(nx + gstride));
         }
-        const long long en = nx * C::EPB + le;
-        if (en < m.E) {
-          int fx, fy, fz;
-          elem_coords(m, en, fx, fy, fz);
-          const double* pu = u + (long long)(fx * P + t0) + (long long)m.Mx * (fy * P + t1) + sxy * (long long)(fz * P);
-#pragma unroll
-          for (int k = 0; k < N; ++k) asm volatile("prefetch.global.L2 [%0];" ::"l"(pu + sxy * k));
-        }
       }
+    }
+    double rn[N];   // next group's u column, in flight during P4-P6
+    if (grp + gstride < ngroups) {
+      load_column(grp + gstride, rn);
+      if (grp + 2 * gstride < ngroups) prefetch_column(grp + 2 * gstride);
     }
     {  // P4: v0 = D^T w0 on x-line (j=t0, k=t1), in place in s0
       double L[N];
@@ -660,7 +577,7 @@ __global__ void __launch_bounds__(V2Cfg<P>::THREADS, V2Cfg<P>::MINB)
       for (int a = 0; a < N; ++a) {
         double s = 0.0;
 #pragma unroll
-        for (int mm = 0; mm < N; ++mm) s = fma(c_D[P - 1][mm * N + a], L[mm], s);
+        for (int mm = 0; mm < N; ++mm) s = fma(dmat<P>(3, mm * N + a + zero), L[mm], s);
         s0[a + N * t0 + N2 * t1] = s;
       }
     }
@@ -673,12 +590,12 @@ __global__ void __launch_bounds__(V2Cfg<P>::THREADS, V2Cfg<P>::MINB)
       for (int b = 0; b < N; ++b) {
         double s = s0[t0 + N * b + N2 * t1];
 #pragma unroll
-        for (int mm = 0; mm < N; ++mm) s = fma(c_D[P - 1][mm * N + b], L[mm], s);
+        for (int mm = 0; mm < N; ++mm) s = fma(dmat<P>(4, mm * N + b + zero), L[mm], s);
         su[t0 + N * b + N2 * t1] = s;
       }
     }
     __syncthreads();
-    if (act) {  // P6: z-line (i=t0, j=t1): v = su + vz, scatter (su column is this thread's own)
+    if (act) {  // P6: z-line (i=t0, j=t1): v = su + vz, scatter (own column of su)
 #pragma unroll
       for (int c = 0; c < N; ++c) {
         bool bnd = false;
@@ -686,6 +603,8 @@ __global__ void __launch_bounds__(V2Cfg<P>::THREADS, V2Cfg<P>::MINB)
         if (!bnd) atomicAdd(v + gcol + sxy * c, su[t + N2 * c] + vz[c]);
       }
     }
+#pragma unroll
+    for (int k = 0; k < N; ++k) ru[k] = rn[k];
   }
 }
 
@@ -698,7 +617,7 @@ template <int P>
 __global__ void __launch_bounds__(256) k_diag(MeshDev m, int bc, const double* __restrict__ G, double* d) {
   constexpr int N = P + 1, N2 = N * N, N3 = N2 * N;
   __shared__ double sD[N * N];
-  for (int t = threadIdx.x; t < N * N; t += blockDim.x) sD[t] = c_D[P - 1][t];
+  for (int t = threadIdx.x; t < N * N; t += blockDim.x) sD[t] = dmat<P>(0, t);
   __syncthreads();
   const long long total = m.E * N3;
   for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
@@ -730,7 +649,7 @@ template <int P>
 __global__ void __launch_bounds__(256) k_load(MeshDev m, double* f) {
   constexpr int N = P + 1, N2 = N * N, N3 = N2 * N;
   __shared__ double sD[N * N], sx[N], sw[N];
-  for (int t = threadIdx.x; t < N * N; t += blockDim.x) sD[t] = c_D[P - 1][t];
+  for (int t = threadIdx.x; t < N * N; t += blockDim.x) sD[t] = dmat<P>(0, t);
   for (int t = threadIdx.x; t < N; t += blockDim.x) { sx[t] = c_x[P - 1][t]; sw[t] = c_w[P - 1][t]; }
   __syncthreads();
   const double pi = 3.14159265358979323846;
@@ -766,11 +685,22 @@ __global__ void __launch_bounds__(256) k_load(MeshDev m, double* f) {
 // ------------------------------------------------------------------------------------------
 // vector kernels that need the lattice
 
-__global__ void k_init(MeshDev m, int bc, const double* __restrict__ u, double bval, double* __restrict__ v) {
-  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < m.N; g += (long long)gridDim.x * blockDim.x) {
-    double val = 0.0;
-    if (bc == 0 && lattice_boundary(m, g)) val = u ? u[g] : bval;
-    v[g] = val;
+// v = (I - M) u (bc 0) or 0 (bc 1).  One warp per lattice row (J, K): the only integer divisions
+// are per row, and each lane writes consecutive doubles of the row.
+__global__ void __launch_bounds__(256) k_init(MeshDev m, int bc, const double* __restrict__ u, double bval,
+                                              double* __restrict__ v) {
+  const int lane = threadIdx.x & 31;
+  const long long rows = (long long)m.My * m.Mz;
+  const long long wstride = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long r = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += wstride) {
+    const int J = (int)(r % m.My), K = (int)(r / m.My);
+    const bool rowb = (bc == 0) && (J == 0 || J == m.My - 1 || K == 0 || K == m.Mz - 1);
+    double* vr = v + r * m.Mx;
+    const double* ur = u ? u + r * m.Mx : nullptr;
+    for (int I = lane; I < m.Mx; I += 32) {
+      const bool b = rowb || (bc == 0 && (I == 0 || I == m.Mx - 1));
+      vr[I] = b ? (ur ? ur[I] : bval) : 0.0;
+    }
   }
 }
 
@@ -860,9 +790,9 @@ __device__ void cta_apply(const MeshDev& m, const double* __restrict__ G, const 
           double g0 = 0, g1 = 0, g2 = 0;
 #pragma unroll
           for (int mm = 0; mm < N; ++mm) {
-            g0 = fma(c_D[P - 1][i * N + mm], ue[mm + N * (j + N * k)], g0);
-            g1 = fma(c_D[P - 1][j * N + mm], ue[i + N * (mm + N * k)], g1);
-            g2 = fma(c_D[P - 1][k * N + mm], ue[i + N * (j + N * mm)], g2);
+            g0 = fma(dmat<P>(0, i * N + mm), ue[mm + N * (j + N * k)], g0);
+            g1 = fma(dmat<P>(0, j * N + mm), ue[i + N * (mm + N * k)], g1);
+            g2 = fma(dmat<P>(0, k * N + mm), ue[i + N * (j + N * mm)], g2);
           }
           const int ij = i + N * j;
           const double G00 = Ge[gofs<N>(0, ij, k)], G01 = Ge[gofs<N>(1, ij, k)], G02 = Ge[gofs<N>(2, ij, k)];
@@ -872,9 +802,9 @@ __device__ void cta_apply(const MeshDev& m, const double* __restrict__ G, const 
           const double w2 = G02 * g0 + G12 * g1 + G22 * g2;
 #pragma unroll
           for (int mm = 0; mm < N; ++mm) {
-            ve[mm + N * (j + N * k)] = fma(c_D[P - 1][i * N + mm], w0, ve[mm + N * (j + N * k)]);
-            ve[i + N * (mm + N * k)] = fma(c_D[P - 1][j * N + mm], w1, ve[i + N * (mm + N * k)]);
-            ve[i + N * (j + N * mm)] = fma(c_D[P - 1][k * N + mm], w2, ve[i + N * (j + N * mm)]);
+            ve[mm + N * (j + N * k)] = fma(dmat<P>(0, i * N + mm), w0, ve[mm + N * (j + N * k)]);
+            ve[i + N * (mm + N * k)] = fma(dmat<P>(0, j * N + mm), w1, ve[i + N * (mm + N * k)]);
+            ve[i + N * (j + N * mm)] = fma(dmat<P>(0, k * N + mm), w2, ve[i + N * (j + N * mm)]);
           }
         }
 #pragma unroll
@@ -972,13 +902,13 @@ cudaError_t launch_geometry(const MeshDev& m, double* G, int* bad, cudaStream_t 
 template <int P, bool DIR>
 static cudaError_t apply_pd(const MeshDev& m, const double* G, const double* u, double* v, cudaStream_t s) {
   if constexpr (P <= 8) {
-    using C = V2Cfg<P>;
+    using C = V4Cfg<P>;
     static int resident = 0;   // blocks per SM of the persistent kernel
     static int num_sms = 0;
     if (!resident) {
-      cudaError_t e = cudaFuncSetAttribute(k_apply_v3<P, DIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+      cudaError_t e = cudaFuncSetAttribute(k_apply_v4<P, DIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
       if (e) return e;
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_apply_v3<P, DIR>, C::THREADS, C::SMEM);
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_apply_v4<P, DIR>, C::THREADS, C::SMEM);
       if (e) return e;
       int dev = 0;
       cudaGetDevice(&dev);
@@ -988,7 +918,7 @@ static cudaError_t apply_pd(const MeshDev& m, const double* G, const double* u, 
     const long long groups = (m.E + C::EPB - 1) / C::EPB;
     long long grid = (long long)resident * num_sms;
     if (grid > groups) grid = groups;
-    k_apply_v3<P, DIR><<<(unsigned)grid, C::THREADS, C::SMEM, s>>>(m, G, u, v, groups);
+    k_apply_v4<P, DIR><<<(unsigned)grid, C::THREADS, C::SMEM, s>>>(m, G, u, v, groups);
     return cudaSuccess;
   }
   using C = ApplyCfg<P>;
@@ -1040,7 +970,7 @@ cudaError_t launch_load(const MeshDev& m, int rhs_id, double* f, cudaStream_t s)
 }
 
 cudaError_t launch_init(const MeshDev& m, int bc, const double* u, double bval, double* v, cudaStream_t s) {
-  k_init<<<grid_for(m.N, 256), 256, 0, s>>>(m, bc, u, bval, v);
+  k_init<<<grid_for((long long)m.My * m.Mz * 32, 256), 256, 0, s>>>(m, bc, u, bval, v);
   return cudaGetLastError();
 }
 
