@@ -66,6 +66,20 @@ __device__ __forceinline__ double dmat(int cp, int idx) {
 template <int N>
 __device__ __forceinline__ int gofs(int c, int ij, int k) { return k * 6 * N * N + c * N * N + ij; }
 
+// Full offset of G(e, c, ij, k).  For p <= 2 (thread-per-element apply) the factors are stored
+// element-interleaved in blocks of 32 elements, [E/32][k][6][n^2][32], so that a warp in which
+// lane = element reads every component with one coalesced 256-byte access.
+template <int P>
+struct GLayout {
+  static constexpr int N = P + 1, N2 = N * N, N3 = N2 * N;
+  static constexpr bool kTPE = (P <= 2);
+  __host__ __device__ static long long padded_elems(long long E) { return kTPE ? ((E + 31) / 32) * 32 : E; }
+  __device__ static long long off(long long e, int c, int ij, int k) {
+    if (kTPE) return (((e >> 5) * 6 * N3) + (long long)(k * 6 + c) * N2 + ij) * 32 + (e & 31);
+    return e * 6 * N3 + gofs<N>(c, ij, k);
+  }
+};
+
 __device__ __forceinline__ void elem_coords(const MeshDev& m, long long e, int& ex, int& ey, int& ez) {
   ex = (int)(e % m.nex);
   long long t = e / m.nex;
@@ -190,12 +204,11 @@ __global__ void __launch_bounds__(256) k_geometry(MeshDev m, double* __restrict_
     double X[3];
     node_pos<P>(m, sx, ex, ey, ez, i, j, k, X);
     double s = sw[i] * sw[j] * sw[k] * coeff_mu(m, X[0], X[1], X[2]) * det;
-    double* Ge = G + e * 6 * N3 + gofs<N>(0, i + N * j, k);
     const int comp[6][2] = {{0, 0}, {0, 1}, {0, 2}, {1, 1}, {1, 2}, {2, 2}};
 #pragma unroll
     for (int c = 0; c < 6; ++c) {
       int a = comp[c][0], b = comp[c][1];
-      Ge[c * N2] = s * (Ji[a][0] * Ji[b][0] + Ji[a][1] * Ji[b][1] + Ji[a][2] * Ji[b][2]);
+      G[GLayout<P>::off(e, c, i + N * j, k)] = s * (Ji[a][0] * Ji[b][0] + Ji[a][1] * Ji[b][1] + Ji[a][2] * Ji[b][2]);
     }
   }
 }
@@ -609,6 +622,93 @@ __global__ void __launch_bounds__(V4Cfg<P>::THREADS, V4Cfg<P>::MINB)
 }
 
 // ------------------------------------------------------------------------------------------
+// K2 apply, thread per element (p <= 2): the whole element (n^3 <= 27 nodes) lives in registers,
+// so there is no shared memory and no barrier; G streams through coalesced element-interleaved
+// loads (GLayout), the gather and the fp64 REDs of neighbouring lanes touch neighbouring nodes.
+
+template <int P, bool DIR>
+__global__ void __launch_bounds__(128) k_apply_tpe(MeshDev m, const double* __restrict__ G,
+                                                   const double* __restrict__ u, double* __restrict__ v) {
+  constexpr int N = P + 1, N2 = N * N, N3 = N2 * N;
+  using GL = GLayout<P>;
+  const long long sxy = (long long)m.Mx * m.My;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < m.E; e += (long long)gridDim.x * blockDim.x) {
+    int ex, ey, ez;
+    elem_coords(m, e, ex, ey, ez);
+    const long long g0 = (long long)(ex * P) + (long long)m.Mx * (ey * P) + sxy * (long long)(ez * P);
+    double ue[N3], ve[N3];
+#pragma unroll
+    for (int c = 0; c < N; ++c)
+#pragma unroll
+      for (int b = 0; b < N; ++b)
+#pragma unroll
+        for (int a = 0; a < N; ++a) {
+          const int l = a + N * (b + N * c);
+          bool bnd = false;
+          if (DIR) {
+            const int I = ex * P + a, J = ey * P + b, K = ez * P + c;
+            bnd = I == 0 || I == m.Mx - 1 || J == 0 || J == m.My - 1 || K == 0 || K == m.Mz - 1;
+          }
+          ue[l] = bnd ? 0.0 : __ldg(u + g0 + a + (long long)m.Mx * b + sxy * c);
+          ve[l] = 0.0;
+        }
+#pragma unroll
+    for (int k = 0; k < N; ++k)
+#pragma unroll
+      for (int j = 0; j < N; ++j)
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          double d0 = 0, d1 = 0, d2 = 0;
+#pragma unroll
+          for (int mm = 0; mm < N; ++mm) {
+            d0 = fma(dmat<P>(0, i * N + mm), ue[mm + N * (j + N * k)], d0);
+            d1 = fma(dmat<P>(0, j * N + mm), ue[i + N * (mm + N * k)], d1);
+            d2 = fma(dmat<P>(0, k * N + mm), ue[i + N * (j + N * mm)], d2);
+          }
+          const int ij = i + N * j;
+          const double G00 = __ldcs(G + GL::off(e, 0, ij, k)), G01 = __ldcs(G + GL::off(e, 1, ij, k));
+          const double G02 = __ldcs(G + GL::off(e, 2, ij, k)), G11 = __ldcs(G + GL::off(e, 3, ij, k));
+          const double G12 = __ldcs(G + GL::off(e, 4, ij, k)), G22 = __ldcs(G + GL::off(e, 5, ij, k));
+          const double w0 = G00 * d0 + G01 * d1 + G02 * d2;
+          const double w1 = G01 * d0 + G11 * d1 + G12 * d2;
+          const double w2 = G02 * d0 + G12 * d1 + G22 * d2;
+#pragma unroll
+          for (int mm = 0; mm < N; ++mm) {
+            ve[mm + N * (j + N * k)] = fma(dmat<P>(0, i * N + mm), w0, ve[mm + N * (j + N * k)]);
+            ve[i + N * (mm + N * k)] = fma(dmat<P>(0, j * N + mm), w1, ve[i + N * (mm + N * k)]);
+            ve[i + N * (j + N * mm)] = fma(dmat<P>(0, k * N + mm), w2, ve[i + N * (j + N * mm)]);
+          }
+        }
+#pragma unroll
+    for (int c = 0; c < N; ++c)
+#pragma unroll
+      for (int b = 0; b < N; ++b)
+#pragma unroll
+        for (int a = 0; a < N; ++a) {
+          bool bnd = false;
+          if (DIR) {
+            const int I = ex * P + a, J = ey * P + b, K = ez * P + c;
+            bnd = I == 0 || I == m.Mx - 1 || J == 0 || J == m.My - 1 || K == 0 || K == m.Mz - 1;
+          }
+          if (!bnd) atomicAdd(v + g0 + a + (long long)m.Mx * b + sxy * c, ve[a + N * (b + N * c)]);
+        }
+  }
+}
+
+// Export of the factors in the canonical layout [E][k][6][n^2] whatever the internal layout.
+template <int P>
+__global__ void k_export_geometry(MeshDev m, const double* __restrict__ G, double* __restrict__ out) {
+  constexpr int N = P + 1, N2 = N * N, N3 = N2 * N;
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < m.E * 6 * N3;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long e = idx / (6 * N3);
+    const int r = (int)(idx - e * 6 * N3);
+    const int k = r / (6 * N2), c = (r / N2) % 6, ij = r % N2;
+    out[idx] = G[GLayout<P>::off(e, c, ij, k)];
+  }
+}
+
+// ------------------------------------------------------------------------------------------
 // K3 diagonal: for node (a,b,c) of element e
 //   sum_i D[i][a]^2 G00(i,b,c) + sum_j D[j][b]^2 G11(a,j,c) + sum_k D[k][c]^2 G22(a,b,k)
 //   + 2 D[a][a] D[b][b] G01(a,b,c) + 2 D[a][a] D[c][c] G02(a,b,c) + 2 D[b][b] D[c][c] G12(a,b,c)
@@ -629,15 +729,15 @@ __global__ void __launch_bounds__(256) k_diag(MeshDev m, int bc, const double* _
     elem_coords(m, e, ex, ey, ez);
     long long g = (long long)(ex * P + a) + (long long)m.Mx * ((long long)(ey * P + b) + (long long)m.My * (ez * P + c));
     if (bc == 0 && lattice_boundary(m, g)) continue;
-    const double* Ge = G + e * 6 * N3;
+    using GL = GLayout<P>;
     double s = 0.0;
-    for (int i = 0; i < N; ++i) s += sD[i * N + a] * sD[i * N + a] * Ge[gofs<N>(0, i + N * b, c)];
-    for (int j = 0; j < N; ++j) s += sD[j * N + b] * sD[j * N + b] * Ge[gofs<N>(3, a + N * j, c)];
-    for (int k = 0; k < N; ++k) s += sD[k * N + c] * sD[k * N + c] * Ge[gofs<N>(5, a + N * b, k)];
+    for (int i = 0; i < N; ++i) s += sD[i * N + a] * sD[i * N + a] * G[GL::off(e, 0, i + N * b, c)];
+    for (int j = 0; j < N; ++j) s += sD[j * N + b] * sD[j * N + b] * G[GL::off(e, 3, a + N * j, c)];
+    for (int k = 0; k < N; ++k) s += sD[k * N + c] * sD[k * N + c] * G[GL::off(e, 5, a + N * b, k)];
     const double da = sD[a * N + a], db = sD[b * N + b], dc = sD[c * N + c];
     const int ab = a + N * b;
-    s += 2.0 * da * db * Ge[gofs<N>(1, ab, c)] + 2.0 * da * dc * Ge[gofs<N>(2, ab, c)] +
-         2.0 * db * dc * Ge[gofs<N>(4, ab, c)];
+    s += 2.0 * da * db * G[GL::off(e, 1, ab, c)] + 2.0 * da * dc * G[GL::off(e, 2, ab, c)] +
+         2.0 * db * dc * G[GL::off(e, 4, ab, c)];
     atomicAdd(d + g, s);
   }
 }
@@ -780,7 +880,6 @@ __device__ void cta_apply(const MeshDev& m, const double* __restrict__ G, const 
           ue[l] = bnd ? 0.0 : __ldcg(x + g);
           ve[l] = 0.0;
         }
-    const double* Ge = G + e * 6 * N3;
 #pragma unroll
     for (int k = 0; k < N; ++k)
 #pragma unroll
@@ -795,8 +894,9 @@ __device__ void cta_apply(const MeshDev& m, const double* __restrict__ G, const 
             g2 = fma(dmat<P>(0, k * N + mm), ue[i + N * (j + N * mm)], g2);
           }
           const int ij = i + N * j;
-          const double G00 = Ge[gofs<N>(0, ij, k)], G01 = Ge[gofs<N>(1, ij, k)], G02 = Ge[gofs<N>(2, ij, k)];
-          const double G11 = Ge[gofs<N>(3, ij, k)], G12 = Ge[gofs<N>(4, ij, k)], G22 = Ge[gofs<N>(5, ij, k)];
+          using GL = GLayout<P>;
+          const double G00 = G[GL::off(e, 0, ij, k)], G01 = G[GL::off(e, 1, ij, k)], G02 = G[GL::off(e, 2, ij, k)];
+          const double G11 = G[GL::off(e, 3, ij, k)], G12 = G[GL::off(e, 4, ij, k)], G22 = G[GL::off(e, 5, ij, k)];
           const double w0 = G00 * g0 + G01 * g1 + G02 * g2;
           const double w1 = G01 * g0 + G11 * g1 + G12 * g2;
           const double w2 = G02 * g0 + G12 * g1 + G22 * g2;
@@ -901,7 +1001,21 @@ cudaError_t launch_geometry(const MeshDev& m, double* G, int* bad, cudaStream_t 
 
 template <int P, bool DIR>
 static cudaError_t apply_pd(const MeshDev& m, const double* G, const double* u, double* v, cudaStream_t s) {
-  if constexpr (P <= 8) {
+  if constexpr (P <= 2) {
+    static int grid = 0;
+    if (!grid) {
+      int per_sm = 0, dev = 0, sms = 0;
+      cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_apply_tpe<P, DIR>, 128, 0);
+      if (e) return e;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      grid = (per_sm > 0 ? per_sm : 1) * sms;
+    }
+    long long blocks = (m.E + 127) / 128;
+    if (blocks > grid) blocks = grid;
+    k_apply_tpe<P, DIR><<<(unsigned)blocks, 128, 0, s>>>(m, G, u, v);
+    return cudaSuccess;
+  } else if constexpr (P <= 8) {
     using C = V4Cfg<P>;
     static int resident = 0;   // blocks per SM of the persistent kernel
     static int num_sms = 0;
@@ -980,6 +1094,17 @@ cudaError_t launch_cheb_update(const MeshDev& m, const double* cur, const double
   k_cheb_update<<<grid_for(m.N, 256), 256, 0, s>>>(m, cur, prev, out, b, y, dinv, c1, c2);
   return cudaGetLastError();
 }
+
+template <int P>
+static void export_geometry_p(const MeshDev& m, const double* G, double* out, cudaStream_t s) {
+  k_export_geometry<P><<<grid_for(m.E * 6 * (P + 1) * (P + 1) * (P + 1), 256), 256, 0, s>>>(m, G, out);
+}
+cudaError_t launch_export_geometry(const MeshDev& m, const double* G, double* out, cudaStream_t s) {
+  SFMG_DISPATCH_P(m.p, export_geometry_p, m, G, out, s);
+  return cudaGetLastError();
+}
+
+long long geometry_elems(int p, long long E) { return p <= 2 ? ((E + 31) / 32) * 32 : E; }
 
 cudaError_t launch_export_maps(const MeshDev& m, int32_t* l2g, uint8_t* mask, uint8_t* col, cudaStream_t s) {
   long long work = m.E * (long long)(m.p + 1) * (m.p + 1) * (m.p + 1);

@@ -60,7 +60,7 @@ static LevelLayout level_layout(const MeshDev& m) {
   const long long n3 = (long long)(m.p + 1) * (m.p + 1) * (m.p + 1);
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off += align_up(bytes); return o; };
-  L.G = take(sizeof(double) * 6 * (size_t)m.E * n3);
+  L.G = take(sizeof(double) * 6 * (size_t)geometry_elems(m.p, m.E) * n3);
   L.dinv = take(sizeof(double) * m.N);
   L.y = take(sizeof(double) * m.N);
   L.t0 = take(sizeof(double) * m.N);
@@ -218,7 +218,7 @@ sfmg_status sfmg_export_colors(sfmg_level lv, uint8_t* d_col, void* stream) {
 }
 sfmg_status sfmg_export_geometry(sfmg_level lv, double* d_G, void* stream) {
   if (!lv || !d_G) return SFMG_E_ARG;
-  CK(cudaMemcpyAsync(d_G, lv->G, sizeof(double) * 6 * lv->E * lv->n3, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+  CK(launch_export_geometry(lv->m, lv->G, d_G, (cudaStream_t)stream));
   return SFMG_OK;
 }
 

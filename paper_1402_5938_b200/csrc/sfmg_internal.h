@@ -82,6 +82,9 @@ cudaError_t launch_load(const MeshDev& m, int rhs_id, double* f, cudaStream_t s)
 cudaError_t launch_cheb_update(const MeshDev& m, const double* cur, const double* prev, double* out,
                                const double* b, double* y, const double* dinv, double c1, double c2,
                                cudaStream_t s);
+cudaError_t launch_export_geometry(const MeshDev& m, const double* G, double* out, cudaStream_t s);
+// elements for which G storage is allocated (p <= 2: rounded up to 32 for the interleaved layout)
+long long geometry_elems(int p, long long E);
 cudaError_t launch_export_maps(const MeshDev& m, int32_t* l2g, uint8_t* mask, uint8_t* col, cudaStream_t s);
 // single-CTA CG on a (small) level: x = A_D^{-1} b to rtol (R13)
 cudaError_t launch_coarse_cg(const MeshDev& m, const double* G, const double* b, double* x, double* r,
