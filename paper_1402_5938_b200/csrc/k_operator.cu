@@ -22,6 +22,7 @@ namespace sfmg {
 constexpr int kDCopies = 5;
 __constant__ double c_D8[8][kDCopies][81];
 __constant__ double c_D16[8][17 * 17];   // p = 9..16
+__constant__ double c_D16c[kDCopies][17 * 17];   // p = 16: per-pass copies as for p <= 8
 __constant__ double c_x[kMaxOrder][17];
 __constant__ double c_w[kMaxOrder][17];
 
@@ -40,6 +41,11 @@ cudaError_t upload_order_tables(int p, cudaStream_t s) {
   } else {
     e = cudaMemcpyToSymbol(c_D16, B.D.data(), sizeof(double) * n * n, sizeof(double) * 17 * 17 * (p - 9));
     if (e) return e;
+    if (p == 16)
+      for (int c = 0; c < kDCopies; ++c) {
+        e = cudaMemcpyToSymbol(c_D16c, B.D.data(), sizeof(double) * n * n, sizeof(double) * 17 * 17 * c);
+        if (e) return e;
+      }
   }
   e = cudaMemcpyToSymbol(c_x, B.x.data(), sizeof(double) * n, sizeof(double) * 17 * (p - 1));
   if (e) return e;
@@ -57,6 +63,7 @@ cudaError_t upload_order_tables(int p, cudaStream_t s) {
 template <int P>
 __device__ __forceinline__ double dmat(int cp, int idx) {
   if constexpr (P <= 8) return c_D8[P - 1][cp][idx];
+  else if constexpr (P == 16) return c_D16c[cp][idx];
   else return c_D16[P - 9][idx];
 }
 
@@ -214,168 +221,7 @@ __global__ void __launch_bounds__(256) k_geometry(MeshDev m, double* __restrict_
 }
 
 // ------------------------------------------------------------------------------------------
-// K2 apply.  Block = EPB elements x (n x n) threads.  Thread t = (t0, t1) of an element owns
-// one 1-D line per phase:
-//   gather   : column (i=t0, j=t1) over k       -> registers ru[] and smem su
-//   P1       : x-line (j=t0, k=t1): g0 = D u     -> s0
-//   P2       : y-line (i=t0, k=t1): g1 = D u     -> s1
-//   P3       : z-line (i=t0, j=t1): g2 = D ru (registers), w = G g (G streamed from HBM,
-//              coalesced over the (i,j) slab), w0 -> s0, w1 -> s1, vz = D^T w2 (registers)
-//   P4       : x-line: v0 = D^T w0 -> su
-//   P5       : y-line: su += D^T w1
-//   P6       : z-line: v = su + vz, RED.ADD into v[g] (interior rows only for bc 0)
-// Each line pass reads n values and does n^2 FMAs, so the shared-memory traffic is ~14 n^3
-// doubles per element against 6 n^4 FMAs.
-
-template <int P>
-struct ApplyCfg {
-  static constexpr int N = P + 1, N2 = N * N, N3 = N2 * N;
-  static constexpr int EPB = (256 / N2) > 0 ? (256 / N2) : 1;
-  static constexpr int THREADS = EPB * N2;
-  static constexpr size_t SMEM = (size_t)EPB * 3 * N3 * sizeof(double);
-};
-
-template <int P, bool DIR>
-__global__ void __launch_bounds__(ApplyCfg<P>::THREADS)
-    k_apply(MeshDev m, const double* __restrict__ G, const double* __restrict__ u, double* __restrict__ v) {
-  using C = ApplyCfg<P>;
-  constexpr int N = C::N, N2 = C::N2, N3 = C::N3;
-  extern __shared__ double smem[];
-  const int le = threadIdx.x / N2;
-  const int t = threadIdx.x - le * N2;
-  const int t0 = t % N, t1 = t / N;
-  const long long e = (long long)blockIdx.x * C::EPB + le;
-  const bool act = e < m.E;
-  double* su = smem + le * 3 * N3;
-  double* s0 = su + N3;
-  double* s1 = s0 + N3;
-
-  int ex = 0, ey = 0, ez = 0;
-  if (act) elem_coords(m, e, ex, ey, ez);
-  const long long sxy = (long long)m.Mx * m.My;
-  const long long gcol = (long long)(ex * P + t0) + (long long)m.Mx * (ey * P + t1) + sxy * (long long)(ez * P);
-  bool bxy = false;
-  if (DIR) {
-    const int I = ex * P + t0, J = ey * P + t1;
-    bxy = (I == 0) || (I == m.Mx - 1) || (J == 0) || (J == m.My - 1);
-  }
-
-  double ru[N];
-#pragma unroll
-  for (int k = 0; k < N; ++k) {
-    double val = 0.0;
-    if (act) {
-      bool bnd = false;
-      if (DIR) { const int K = ez * P + k; bnd = bxy || K == 0 || K == m.Mz - 1; }
-      if (!bnd) val = __ldg(u + gcol + sxy * k);
-    }
-    ru[k] = val;
-    su[t0 + N * t1 + N2 * k] = val;
-  }
-  __syncthreads();
-
-  {  // P1: x-derivative on line (j=t0, k=t1)
-    double L[N];
-#pragma unroll
-    for (int mm = 0; mm < N; ++mm) L[mm] = su[mm + N * t0 + N2 * t1];
-#pragma unroll
-    for (int i = 0; i < N; ++i) {
-      double s = 0.0;
-#pragma unroll
-      for (int mm = 0; mm < N; ++mm) s = fma(dmat<P>(0, i * N + mm), L[mm], s);
-      s0[i + N * t0 + N2 * t1] = s;
-    }
-  }
-  {  // P2: y-derivative on line (i=t0, k=t1)
-    double L[N];
-#pragma unroll
-    for (int mm = 0; mm < N; ++mm) L[mm] = su[t0 + N * mm + N2 * t1];
-#pragma unroll
-    for (int j = 0; j < N; ++j) {
-      double s = 0.0;
-#pragma unroll
-      for (int mm = 0; mm < N; ++mm) s = fma(dmat<P>(0, j * N + mm), L[mm], s);
-      s1[t0 + N * j + N2 * t1] = s;
-    }
-  }
-  __syncthreads();
-
-  double vz[N];
-  {  // P3: z-derivative in registers, pointwise metric product, z-transpose in registers
-    const double* Ge = G + (act ? e : 0) * 6 * N3 + t0 + N * t1;
-    double w2[N];
-#pragma unroll
-    for (int k = 0; k < N; ++k) {
-      double g2 = 0.0;
-#pragma unroll
-      for (int mm = 0; mm < N; ++mm) g2 = fma(dmat<P>(0, k * N + mm), ru[mm], g2);
-      const int idx = t0 + N * t1 + N2 * k;
-      const double g0 = s0[idx], g1 = s1[idx];
-      double G00 = 0, G01 = 0, G02 = 0, G11 = 0, G12 = 0, G22 = 0;
-      if (act) {
-        G00 = __ldcs(Ge + gofs<N>(0, 0, k));
-        G01 = __ldcs(Ge + gofs<N>(1, 0, k));
-        G02 = __ldcs(Ge + gofs<N>(2, 0, k));
-        G11 = __ldcs(Ge + gofs<N>(3, 0, k));
-        G12 = __ldcs(Ge + gofs<N>(4, 0, k));
-        G22 = __ldcs(Ge + gofs<N>(5, 0, k));
-      }
-      s0[idx] = G00 * g0 + G01 * g1 + G02 * g2;
-      s1[idx] = G01 * g0 + G11 * g1 + G12 * g2;
-      w2[k] = G02 * g0 + G12 * g1 + G22 * g2;
-    }
-#pragma unroll
-    for (int c = 0; c < N; ++c) {
-      double s = 0.0;
-#pragma unroll
-      for (int k = 0; k < N; ++k) s = fma(dmat<P>(0, k * N + c), w2[k], s);
-      vz[c] = s;
-    }
-  }
-  __syncthreads();
-
-  {  // P4: v0 = D^T w0 on x-line (j=t0, k=t1) -> su
-    double L[N];
-#pragma unroll
-    for (int mm = 0; mm < N; ++mm) L[mm] = s0[mm + N * t0 + N2 * t1];
-#pragma unroll
-    for (int a = 0; a < N; ++a) {
-      double s = 0.0;
-#pragma unroll
-      for (int mm = 0; mm < N; ++mm) s = fma(dmat<P>(0, mm * N + a), L[mm], s);
-      su[a + N * t0 + N2 * t1] = s;
-    }
-  }
-  __syncthreads();
-  {  // P5: su += D^T w1 on y-line (i=t0, k=t1)
-    double L[N];
-#pragma unroll
-    for (int mm = 0; mm < N; ++mm) L[mm] = s1[t0 + N * mm + N2 * t1];
-#pragma unroll
-    for (int b = 0; b < N; ++b) {
-      double s = 0.0;
-#pragma unroll
-      for (int mm = 0; mm < N; ++mm) s = fma(dmat<P>(0, mm * N + b), L[mm], s);
-      su[t0 + N * b + N2 * t1] += s;
-    }
-  }
-  __syncthreads();
-  if (act) {  // P6: z-line (i=t0, j=t1): assemble and scatter
-#pragma unroll
-    for (int c = 0; c < N; ++c) {
-      bool bnd = false;
-      if (DIR) { const int K = ez * P + c; bnd = bxy || K == 0 || K == m.Mz - 1; }
-      if (!bnd) atomicAdd(v + gcol + sxy * c, su[t0 + N * t1 + N2 * c] + vz[c]);
-    }
-  }
-}
-
-// ------------------------------------------------------------------------------------------
-// K2 apply, v2 (p <= 8): the block's geometric factors (EPB consecutive elements, one contiguous
-// block of 48 EPB n^3 bytes) are fetched into shared memory by ONE TMA bulk copy
-// (cp.async.bulk ... mbarrier::complete_tx) issued at block start, so the HBM stream overlaps the
-// gather and the first two derivative passes; blocks are small (<= ~50 KB smem) so 4 co-reside
-// per SM and keep >= 2 copies in flight.  Work arrays: 2 n^3 per element (line passes in place).
+// TMA / mbarrier / cp.async helpers (inline PTX).
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 
@@ -410,16 +256,20 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 
 
 // ------------------------------------------------------------------------------------------
-// K2 apply, v4 (p <= 8): persistent, software-pipelined across element groups.
-// Block = EPB elements x (n x n) threads; each block walks groups grp = blockIdx.x, + gridDim.x...
-//  * geometric factors: one TMA bulk copy (cp.async.bulk + mbarrier complete_tx) per group into
-//    shared memory, issued for group g+1 as soon as P3 of group g has consumed the buffer, plus a
-//    TMA L2 prefetch (cp.async.bulk.prefetch.L2) of group g+2, so every resident block keeps its
-//    next-but-one group's factors in flight from HBM;
-//  * u gather: per-thread cp.async (LDGSTS, zero-fill for Dirichlet/inactive nodes) of the next
-//    group's column into a second u buffer, also issued after P3, so the gather latency of group
-//    g+1 hides behind P4-P6 of group g.
-// Smem per element: 6 n^3 (G) + 3 n^3 (s0, two u/line buffers) doubles.
+// K2 apply, v4 (p >= 3): persistent, software-pipelined across element groups.
+// Block = EPB elements x (n x n) threads; thread t = (t0, t1) of an element owns one 1-D line per
+// pass: P1 x-lines g0 = D u -> s0; P2 y-lines g1 = D u (in place); P3 z-lines in registers:
+// g2 = D u, w = G g, w0 -> s0, w1 -> su, vz = D^T w2; P4 x-lines v0 = D^T w0 (in place);
+// P5 y-lines su = D^T w1 + v0; P6 z-lines v = su + vz, fp64 RED into v.  Each line pass reads n
+// values and does n^2 FMAs (D from __constant__ via uniform registers).
+// Each block walks groups grp = blockIdx.x, + gridDim.x, ...:
+//  * p <= 8 (GS): one TMA bulk copy (cp.async.bulk + mbarrier complete_tx) of the group's factors
+//    into smem, issued for group g+1 as soon as P3 of group g has consumed the buffer;
+//  * p >= 9: the factors are read in P3 straight from L2 with a 3-slice register ring;
+//  * both: a TMA L2 prefetch (cp.async.bulk.prefetch.L2) of group g+2's factors, and the u column
+//    of group g+1 loaded into registers during P4-P6 (group g+2's column prefetched to L2), so HBM
+//    always has the next-but-one group of every resident block in flight.
+// Smem per element: 2 n^3 doubles (+ 6 n^3 staged factors when GS).
 
 __device__ __forceinline__ void cp_async8(double* dst, const double* src, unsigned src_bytes) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes)
@@ -428,31 +278,37 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src, unsign
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-template <int P>
+// GS = true : the group's factors are staged in smem by one TMA bulk copy (p <= 8 fits).
+// GS = false: P3 reads the factors straight from L2 into registers (three k-slices in flight);
+//             the whole next-but-one element is TMA-prefetched into L2 (p >= 9: G of one element is
+//             up to 236 KB and cannot be staged).
+template <int P, bool GS>
 struct V4Cfg {
   static constexpr int N = P + 1, N2 = N * N, N3 = N2 * N;
-  static constexpr int EPB_SMEM = 52000 / (64 * N3) > 0 ? 52000 / (64 * N3) : 1;
+  static constexpr int PER_ELEM = (GS ? 8 : 2) * N3 * 8;   // smem bytes per element
+  static constexpr int EPB_SMEM = 52000 / PER_ELEM > 0 ? 52000 / PER_ELEM : 1;
   static constexpr int EPB_THR = 256 / N2 > 0 ? 256 / N2 : 1;
   static constexpr int EPB = EPB_SMEM < EPB_THR ? EPB_SMEM : EPB_THR;
   static constexpr int THREADS = EPB * N2;
-  static constexpr size_t SMEM = (size_t)EPB * 8 * N3 * sizeof(double) + 16;
-  static constexpr int MINB = (227 * 1024) / (SMEM + 1024) < 8 ? (227 * 1024) / (SMEM + 1024) : 8;
+  static constexpr size_t SMEM = (size_t)EPB * PER_ELEM + 16;
+  static constexpr int MINB_SMEM = (227 * 1024) / (SMEM + 1024) < 8 ? (227 * 1024) / (SMEM + 1024) : 8;
+  static constexpr int MINB = GS ? MINB_SMEM : (P >= 12 ? 1 : 2);
 };
 
-template <int P, bool DIR>
-__global__ void __launch_bounds__(V4Cfg<P>::THREADS, V4Cfg<P>::MINB)
+template <int P, bool DIR, bool GS>
+__global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
     k_apply_v4(MeshDev m, const double* __restrict__ G, const double* __restrict__ u, double* __restrict__ v,
                long long ngroups) {
-  using C = V4Cfg<P>;
+  using C = V4Cfg<P, GS>;
   constexpr int N = C::N, N2 = C::N2, N3 = C::N3;
   extern __shared__ __align__(128) double smem[];
-  double* sG = smem;                                   // [EPB][k][6][n^2]
+  double* sG = smem;                                   // [EPB][k][6][n^2] (GS)
   const int le = threadIdx.x / N2;
   const int t = threadIdx.x - le * N2;
   const int t0 = t % N, t1 = t / N;
-  double* s0 = smem + C::EPB * 6 * N3 + le * 2 * N3;   // per element: s0, su
+  double* s0 = smem + (GS ? C::EPB * 6 * N3 : 0) + le * 2 * N3;   // per element: s0, su
   double* su = s0 + N3;
-  uint64_t* bar = (uint64_t*)(smem + C::EPB * 8 * N3);
+  uint64_t* bar = (uint64_t*)(smem + C::EPB * (GS ? 8 : 2) * N3);
   const double* gE = sG + le * 6 * N3;
   const long long sxy = (long long)m.Mx * m.My;
   const long long gstride = gridDim.x;
@@ -461,8 +317,12 @@ __global__ void __launch_bounds__(V4Cfg<P>::THREADS, V4Cfg<P>::MINB)
     if (nel > C::EPB) nel = C::EPB;
     return (unsigned)(nel * 6 * N3 * sizeof(double));
   };
-  // this thread's u column of group g (M u: zero outside the element / on Dirichlet nodes, R4),
-  // loaded into registers one group ahead; and an L2 prefetch of the column of group g
+  auto prefetch_group_l2 = [&](long long g) {   // TMA L2 prefetch in <= 64 KB pieces
+    const char* src = (const char*)(G + g * C::EPB * 6 * N3);
+    const unsigned total = group_bytes(g);
+    for (unsigned o = 0; o < total; o += 65536u) bulk_prefetch_l2(src + o, total - o < 65536u ? total - o : 65536u);
+  };
+  // this thread's u column of group g (M u: zero outside the element / on Dirichlet nodes, R4)
   auto load_column = [&](long long g, double (&r)[N]) {
     const long long e = g * C::EPB + le;
     const bool act = e < m.E;
@@ -496,13 +356,16 @@ __global__ void __launch_bounds__(V4Cfg<P>::THREADS, V4Cfg<P>::MINB)
   if (grp < ngroups) load_column(grp, ru);
   if (grp + gstride < ngroups) prefetch_column(grp + gstride);
   if (threadIdx.x == 0) {
-    mbar_init(bar, 1);
-    if (grp < ngroups) bulk_load(sG, G + grp * C::EPB * 6 * N3, group_bytes(grp), bar);
-    if (grp + gstride < ngroups) bulk_prefetch_l2(G + (grp + gstride) * C::EPB * 6 * N3, group_bytes(grp + gstride));
+    if (GS) {
+      mbar_init(bar, 1);
+      if (grp < ngroups) bulk_load(sG, G + grp * C::EPB * 6 * N3, group_bytes(grp), bar);
+    } else if (grp < ngroups) {
+      prefetch_group_l2(grp);
+    }
+    if (grp + gstride < ngroups) prefetch_group_l2(grp + gstride);
   }
   unsigned phase = 0;
   for (; grp < ngroups; grp += gstride) {
-    // 0 at run time, but loop-variant: stops ptxas from hoisting the D loads out of the loop
     constexpr int zero = 0;
     const long long e = grp * C::EPB + le;
     const bool act = e < m.E;
@@ -513,6 +376,14 @@ __global__ void __launch_bounds__(V4Cfg<P>::THREADS, V4Cfg<P>::MINB)
     if (DIR) {
       const int I = ex * P + t0, J = ey * P + t1;
       bxy = (I == 0) || (I == m.Mx - 1) || (J == 0) || (J == m.My - 1);
+    }
+    const double* Gg = G + (act ? e : 0) * 6 * N3 + t;   // GS == false: this thread's factor column
+    double gb[3][6];                                        // GS == false: k-slice ring in registers
+    if (!GS) {
+#pragma unroll
+      for (int kk = 0; kk < 2 && kk < N; ++kk)
+#pragma unroll
+        for (int c = 0; c < 6; ++c) gb[kk][c] = __ldcs(Gg + gofs<N>(c, 0, kk));
     }
 #pragma unroll
     for (int k = 0; k < N; ++k) su[t + N2 * k] = ru[k];
@@ -543,21 +414,33 @@ __global__ void __launch_bounds__(V4Cfg<P>::THREADS, V4Cfg<P>::MINB)
       }
     }
     __syncthreads();
-    mbar_wait(bar, phase);
-    phase ^= 1u;
+    if (GS) {
+      mbar_wait(bar, phase);
+      phase ^= 1u;
+    }
     double vz[N];
-    {  // P3: g2 in registers, w = G g (G from smem), vz += D^T w2
+    {  // P3: g2 in registers, w = G g, vz += D^T w2
 #pragma unroll
       for (int c = 0; c < N; ++c) vz[c] = 0.0;
 #pragma unroll
       for (int k = 0; k < N; ++k) {
+        double G00, G01, G02, G11, G12, G22;
+        if (GS) {
+          const double* Gk = gE + gofs<N>(0, t, k);
+          G00 = Gk[0]; G01 = Gk[N2]; G02 = Gk[2 * N2]; G11 = Gk[3 * N2]; G12 = Gk[4 * N2]; G22 = Gk[5 * N2];
+        } else {
+          if (k + 2 < N) {
+#pragma unroll
+            for (int c = 0; c < 6; ++c) gb[(k + 2) % 3][c] = __ldcs(Gg + gofs<N>(c, 0, k + 2));
+          }
+          G00 = gb[k % 3][0]; G01 = gb[k % 3][1]; G02 = gb[k % 3][2];
+          G11 = gb[k % 3][3]; G12 = gb[k % 3][4]; G22 = gb[k % 3][5];
+        }
         double g2 = 0.0;
 #pragma unroll
         for (int mm = 0; mm < N; ++mm) g2 = fma(dmat<P>(2, k * N + mm + zero), ru[mm], g2);
         const int idx = t + N2 * k;
         const double g0 = s0[idx], g1 = su[idx];
-        const double* Gk = gE + gofs<N>(0, t, k);
-        const double G00 = Gk[0], G01 = Gk[N2], G02 = Gk[2 * N2], G11 = Gk[3 * N2], G12 = Gk[4 * N2], G22 = Gk[5 * N2];
         s0[idx] = G00 * g0 + G01 * g1 + G02 * g2;
         su[idx] = G01 * g0 + G11 * g1 + G12 * g2;
         const double w2 = G02 * g0 + G12 * g1 + G22 * g2;
@@ -566,15 +449,14 @@ __global__ void __launch_bounds__(V4Cfg<P>::THREADS, V4Cfg<P>::MINB)
       }
     }
     __syncthreads();
-    {  // factors consumed: next group's G (TMA from L2) and u column (cp.async); G of g+2 to L2
+    {  // factors consumed: next group's G (TMA from L2) and the L2 prefetch of the group after
       const long long nx = grp + gstride;
-      if (nx < ngroups) {
-        if (threadIdx.x == 0) {
+      if (nx < ngroups && threadIdx.x == 0) {
+        if (GS) {
           fence_proxy_async_smem();
           bulk_load(sG, G + nx * C::EPB * 6 * N3, group_bytes(nx), bar);
-          if (nx + gstride < ngroups)
-            bulk_prefetch_l2(G + (nx + gstride) * C::EPB * 6 * N3, group_bytes(nx + gstride));
         }
+        if (nx + gstride < ngroups) prefetch_group_l2(nx + gstride);
       }
     }
     double rn[N];   // next group's u column, in flight during P4-P6
@@ -1015,14 +897,15 @@ static cudaError_t apply_pd(const MeshDev& m, const double* G, const double* u, 
     if (blocks > grid) blocks = grid;
     k_apply_tpe<P, DIR><<<(unsigned)blocks, 128, 0, s>>>(m, G, u, v);
     return cudaSuccess;
-  } else if constexpr (P <= 8) {
-    using C = V4Cfg<P>;
+  } else {
+    constexpr bool GS = (P <= 8);
+    using C = V4Cfg<P, GS>;
     static int resident = 0;   // blocks per SM of the persistent kernel
     static int num_sms = 0;
     if (!resident) {
-      cudaError_t e = cudaFuncSetAttribute(k_apply_v4<P, DIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+      cudaError_t e = cudaFuncSetAttribute(k_apply_v4<P, DIR, GS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
       if (e) return e;
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_apply_v4<P, DIR>, C::THREADS, C::SMEM);
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_apply_v4<P, DIR, GS>, C::THREADS, C::SMEM);
       if (e) return e;
       int dev = 0;
       cudaGetDevice(&dev);
@@ -1032,19 +915,9 @@ static cudaError_t apply_pd(const MeshDev& m, const double* G, const double* u, 
     const long long groups = (m.E + C::EPB - 1) / C::EPB;
     long long grid = (long long)resident * num_sms;
     if (grid > groups) grid = groups;
-    k_apply_v4<P, DIR><<<(unsigned)grid, C::THREADS, C::SMEM, s>>>(m, G, u, v, groups);
+    k_apply_v4<P, DIR, GS><<<(unsigned)grid, C::THREADS, C::SMEM, s>>>(m, G, u, v, groups);
     return cudaSuccess;
   }
-  using C = ApplyCfg<P>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_apply<P, DIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
-    if (e) return e;
-    attr = true;
-  }
-  const long long blocks = (m.E + C::EPB - 1) / C::EPB;
-  k_apply<P, DIR><<<(unsigned)blocks, C::THREADS, C::SMEM, s>>>(m, G, u, v);
-  return cudaSuccess;
 }
 template <int P>
 static void apply_p(const MeshDev& m, int bc, const double* G, const double* u, double* v, cudaStream_t s,
