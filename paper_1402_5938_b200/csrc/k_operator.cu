@@ -16,55 +16,114 @@
 
 namespace sfmg {
 
-// D for p <= 8 in 5 identical copies, one per line pass of the apply kernel: each pass then reads
-// its own constant addresses, so ptxas reloads D per pass (LDCU into uniform registers feeding
-// DFMA) instead of keeping all n^2 values live in the register file across passes.
+// Constant-memory tables (packed per order; 43 KB in total):
+//  * c_Dc: D[i][m] = ell_m'(xhat_i) of every order; odd p <= 7 keep 5 identical copies, one per line
+//    pass of the apply kernel, so each pass reads its own constant addresses and ptxas reloads D per
+//    pass (LDCU into uniform registers feeding DFMA) instead of keeping all n^2 values live in the
+//    register file across passes (which produced R2UR/IMAD juggling and spills).
+//  * c_EO: even p >= 4, the even-odd split of D (and D^T), 6 copies (one per line-pass use).  LGL
+//    nodes are symmetric, so D is centro-antisymmetric, D[n-1-i][n-1-m] = -D[i][m]; with
+//    e_m = L_m + L_{n-1-m}, o_m = L_m - L_{n-1-m} (m < c = p/2):
+//      (D L)_i       = S_i + T_i,   (D L)_{n-1-i} = S_i - T_i   (i < c),   (D L)_c = sum_m D[c][m] o_m
+//      S_i = sum_m A[i][m] o_m,  A = (D[i][m] - D[i][n-1-m]) / 2
+//      T_i = sum_m B[i][m] e_m + D[i][c] L_c,  B = (D[i][m] + D[i][n-1-m]) / 2
+//    which is the same product with 2c^2 + 6c instead of n^2 fp64 operations (-31 % at p = 8,
+//    -39 % at p = 16) and half the constants.
+//  * c_xw: LGL nodes and weights of every order.
 constexpr int kDCopies = 5;
-__constant__ double c_D8[8][kDCopies][81];
-__constant__ double c_D16[8][17 * 17];   // p = 9..16
-__constant__ double c_D16c[kDCopies][17 * 17];   // p = 16: per-pass copies as for p <= 8
-__constant__ double c_x[kMaxOrder][17];
-__constant__ double c_w[kMaxOrder][17];
+constexpr int dcopies(int P) { return (P % 2 == 1 && P <= 7) ? kDCopies : 1; }
+constexpr int dOffset(int P) {
+  int s = 0;
+  for (int q = 1; q < P; ++q) s += dcopies(q) * (q + 1) * (q + 1);
+  return s;
+}
+constexpr int eoSize(int P) { return 2 * (P / 2) * (P / 2) + 2 * (P / 2); }
+constexpr int eoOffset(int P) {
+  int s = 0;
+  for (int q = 4; q < P; q += 2) s += 6 * eoSize(q);
+  return s;
+}
+constexpr int xOffset(int P) {
+  int s = 0;
+  for (int q = 1; q < P; ++q) s += q + 1;
+  return s;
+}
+__constant__ double c_Dc[dOffset(kMaxOrder + 1)];
+__constant__ double c_EO[eoOffset(kMaxOrder + 2)];
+__constant__ double c_xw[2][xOffset(kMaxOrder + 1)];
 
 static bool g_uploaded[kMaxOrder + 1];
 
 cudaError_t upload_order_tables(int p, cudaStream_t s) {
+  (void)s;
   if (g_uploaded[p]) return cudaSuccess;
   Basis1D B = make_basis(p);
   const int n = p + 1;
   cudaError_t e;
-  if (p <= 8) {
-    for (int c = 0; c < kDCopies; ++c) {
-      e = cudaMemcpyToSymbol(c_D8, B.D.data(), sizeof(double) * n * n, sizeof(double) * 81 * (kDCopies * (p - 1) + c));
-      if (e) return e;
-    }
-  } else {
-    e = cudaMemcpyToSymbol(c_D16, B.D.data(), sizeof(double) * n * n, sizeof(double) * 17 * 17 * (p - 9));
+  for (int c = 0; c < dcopies(p); ++c) {
+    e = cudaMemcpyToSymbol(c_Dc, B.D.data(), sizeof(double) * n * n, sizeof(double) * (dOffset(p) + c * n * n));
     if (e) return e;
-    if (p == 16)
-      for (int c = 0; c < kDCopies; ++c) {
-        e = cudaMemcpyToSymbol(c_D16c, B.D.data(), sizeof(double) * n * n, sizeof(double) * 17 * 17 * c);
-        if (e) return e;
-      }
   }
-  e = cudaMemcpyToSymbol(c_x, B.x.data(), sizeof(double) * n, sizeof(double) * 17 * (p - 1));
+  if (p % 2 == 0 && p >= 4) {
+    const int c = p / 2;
+    std::vector<double> tab(6 * eoSize(p));
+    for (int set = 0; set < 6; ++set) {
+      auto M = [&](int i, int m) { return set < 3 ? B.D[i * n + m] : B.D[m * n + i]; };   // D or D^T
+      double* t = tab.data() + set * eoSize(p);
+      for (int i = 0; i < c; ++i)
+        for (int m = 0; m < c; ++m) {
+          t[i * c + m] = 0.5 * (M(i, m) - M(i, n - 1 - m));
+          t[c * c + i * c + m] = 0.5 * (M(i, m) + M(i, n - 1 - m));
+        }
+      for (int i = 0; i < c; ++i) t[2 * c * c + i] = M(i, c);
+      for (int m = 0; m < c; ++m) t[2 * c * c + c + m] = M(c, m);
+    }
+    e = cudaMemcpyToSymbol(c_EO, tab.data(), sizeof(double) * tab.size(), sizeof(double) * eoOffset(p));
+    if (e) return e;
+  }
+  e = cudaMemcpyToSymbol(c_xw, B.x.data(), sizeof(double) * n, sizeof(double) * xOffset(p));
   if (e) return e;
-  e = cudaMemcpyToSymbol(c_w, B.w.data(), sizeof(double) * n, sizeof(double) * 17 * (p - 1));
+  e = cudaMemcpyToSymbol(c_xw, B.w.data(), sizeof(double) * n, sizeof(double) * (xOffset(kMaxOrder + 1) + xOffset(p)));
   if (e) return e;
   g_uploaded[p] = true;
-  (void)s;
   return cudaSuccess;
 }
 
 // ------------------------------------------------------------------------------------------
 // small device helpers
 
-// D[i][m] = ell_m'(xhat_i) of order P, copy `cp` (p <= 8), flat index i * (P+1) + m
+// D[i][m] of order P, copy `cp` (odd p <= 7 only; other orders keep one copy), idx = i (P+1) + m
 template <int P>
 __device__ __forceinline__ double dmat(int cp, int idx) {
-  if constexpr (P <= 8) return c_D8[P - 1][cp][idx];
-  else if constexpr (P == 16) return c_D16c[cp][idx];
-  else return c_D16[P - 9][idx];
+  return c_Dc[dOffset(P) + (dcopies(P) > 1 ? cp : 0) * (P + 1) * (P + 1) + idx];
+}
+
+// out = M L for one 1-D line, M = D (SET 0..2) or D^T (SET 3..5), in the even-odd form above.
+template <int P, int SET>
+__device__ __forceinline__ void eo_line(const double (&L)[P + 1], double (&out)[P + 1]) {
+  constexpr int N = P + 1, c = P / 2;
+  constexpr int base = eoOffset(P) + SET * eoSize(P);
+  double ev[c], od[c];
+#pragma unroll
+  for (int m = 0; m < c; ++m) {
+    ev[m] = L[m] + L[N - 1 - m];
+    od[m] = L[m] - L[N - 1 - m];
+  }
+#pragma unroll
+  for (int i = 0; i < c; ++i) {
+    double S = 0.0, T = c_EO[base + 2 * c * c + i] * L[c];
+#pragma unroll
+    for (int m = 0; m < c; ++m) {
+      S = fma(c_EO[base + i * c + m], od[m], S);
+      T = fma(c_EO[base + c * c + i * c + m], ev[m], T);
+    }
+    out[i] = S + T;
+    out[N - 1 - i] = S - T;
+  }
+  double M = 0.0;
+#pragma unroll
+  for (int m = 0; m < c; ++m) M = fma(c_EO[base + 2 * c * c + c + m], od[m], M);
+  out[c] = M;
 }
 
 // Layout of the geometric factors, slice-major per element: G[e][k][c][j][i], c in (00,01,02,11,
@@ -181,7 +240,7 @@ __global__ void __launch_bounds__(256) k_geometry(MeshDev m, double* __restrict_
   constexpr int N = P + 1, N2 = N * N, N3 = N2 * N;
   __shared__ double sD[N * N], sx[N], sw[N];
   for (int t = threadIdx.x; t < N * N; t += blockDim.x) sD[t] = dmat<P>(0, t);
-  for (int t = threadIdx.x; t < N; t += blockDim.x) { sx[t] = c_x[P - 1][t]; sw[t] = c_w[P - 1][t]; }
+  for (int t = threadIdx.x; t < N; t += blockDim.x) { sx[t] = c_xw[0][xOffset(P) + t]; sw[t] = c_xw[1][xOffset(P) + t]; }
   __syncthreads();
   const long long total = m.E * N3;
   for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
@@ -301,6 +360,7 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
                long long ngroups) {
   using C = V4Cfg<P, GS>;
   constexpr int N = C::N, N2 = C::N2, N3 = C::N3;
+  constexpr bool EO = (P % 2 == 0) && P >= 4;   // even-odd line products
   extern __shared__ __align__(128) double smem[];
   double* sG = smem;                                   // [EPB][k][6][n^2] (GS)
   const int le = threadIdx.x / N2;
@@ -392,12 +452,19 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
       double L[N];
 #pragma unroll
       for (int mm = 0; mm < N; ++mm) L[mm] = su[mm + N * t0 + N2 * t1];
+      if constexpr (EO) {
+        double o[N];
+        eo_line<P, 0>(L, o);
 #pragma unroll
-      for (int i = 0; i < N; ++i) {
-        double s = 0.0;
+        for (int i = 0; i < N; ++i) s0[i + N * t0 + N2 * t1] = o[i];
+      } else {
 #pragma unroll
-        for (int mm = 0; mm < N; ++mm) s = fma(dmat<P>(0, i * N + mm + zero), L[mm], s);
-        s0[i + N * t0 + N2 * t1] = s;
+        for (int i = 0; i < N; ++i) {
+          double s = 0.0;
+#pragma unroll
+          for (int mm = 0; mm < N; ++mm) s = fma(dmat<P>(0, i * N + mm + zero), L[mm], s);
+          s0[i + N * t0 + N2 * t1] = s;
+        }
       }
     }
     __syncthreads();
@@ -405,12 +472,19 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
       double L[N];
 #pragma unroll
       for (int mm = 0; mm < N; ++mm) L[mm] = su[t0 + N * mm + N2 * t1];
+      if constexpr (EO) {
+        double o[N];
+        eo_line<P, 1>(L, o);
 #pragma unroll
-      for (int j = 0; j < N; ++j) {
-        double s = 0.0;
+        for (int j = 0; j < N; ++j) su[t0 + N * j + N2 * t1] = o[j];
+      } else {
 #pragma unroll
-        for (int mm = 0; mm < N; ++mm) s = fma(dmat<P>(1, j * N + mm + zero), L[mm], s);
-        su[t0 + N * j + N2 * t1] = s;
+        for (int j = 0; j < N; ++j) {
+          double s = 0.0;
+#pragma unroll
+          for (int mm = 0; mm < N; ++mm) s = fma(dmat<P>(1, j * N + mm + zero), L[mm], s);
+          su[t0 + N * j + N2 * t1] = s;
+        }
       }
     }
     __syncthreads();
@@ -419,9 +493,19 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
       phase ^= 1u;
     }
     double vz[N];
-    {  // P3: g2 in registers, w = G g, vz += D^T w2
+    {  // P3: g2 = D u on the z-line in registers, w = G g, vz = D^T w2
+      double g2a[N];   // g2 for every k, then overwritten by w2
+      if constexpr (EO) {
+        eo_line<P, 2>(ru, g2a);
+      } else {
 #pragma unroll
-      for (int c = 0; c < N; ++c) vz[c] = 0.0;
+        for (int k = 0; k < N; ++k) {
+          double g2 = 0.0;
+#pragma unroll
+          for (int mm = 0; mm < N; ++mm) g2 = fma(dmat<P>(2, k * N + mm + zero), ru[mm], g2);
+          g2a[k] = g2;
+        }
+      }
 #pragma unroll
       for (int k = 0; k < N; ++k) {
         double G00, G01, G02, G11, G12, G22;
@@ -436,16 +520,22 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
           G00 = gb[k % 3][0]; G01 = gb[k % 3][1]; G02 = gb[k % 3][2];
           G11 = gb[k % 3][3]; G12 = gb[k % 3][4]; G22 = gb[k % 3][5];
         }
-        double g2 = 0.0;
-#pragma unroll
-        for (int mm = 0; mm < N; ++mm) g2 = fma(dmat<P>(2, k * N + mm + zero), ru[mm], g2);
         const int idx = t + N2 * k;
-        const double g0 = s0[idx], g1 = su[idx];
+        const double g0 = s0[idx], g1 = su[idx], g2 = g2a[k];
         s0[idx] = G00 * g0 + G01 * g1 + G02 * g2;
         su[idx] = G01 * g0 + G11 * g1 + G12 * g2;
-        const double w2 = G02 * g0 + G12 * g1 + G22 * g2;
+        g2a[k] = G02 * g0 + G12 * g1 + G22 * g2;
+      }
+      if constexpr (EO) {
+        eo_line<P, 3>(g2a, vz);
+      } else {
 #pragma unroll
-        for (int c = 0; c < N; ++c) vz[c] = fma(dmat<P>(2, k * N + c + zero), w2, vz[c]);
+        for (int c = 0; c < N; ++c) {
+          double s = 0.0;
+#pragma unroll
+          for (int k = 0; k < N; ++k) s = fma(dmat<P>(2, k * N + c + zero), g2a[k], s);
+          vz[c] = s;
+        }
       }
     }
     __syncthreads();
@@ -468,12 +558,19 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
       double L[N];
 #pragma unroll
       for (int mm = 0; mm < N; ++mm) L[mm] = s0[mm + N * t0 + N2 * t1];
+      if constexpr (EO) {
+        double o[N];
+        eo_line<P, 4>(L, o);
 #pragma unroll
-      for (int a = 0; a < N; ++a) {
-        double s = 0.0;
+        for (int a = 0; a < N; ++a) s0[a + N * t0 + N2 * t1] = o[a];
+      } else {
 #pragma unroll
-        for (int mm = 0; mm < N; ++mm) s = fma(dmat<P>(3, mm * N + a + zero), L[mm], s);
-        s0[a + N * t0 + N2 * t1] = s;
+        for (int a = 0; a < N; ++a) {
+          double s = 0.0;
+#pragma unroll
+          for (int mm = 0; mm < N; ++mm) s = fma(dmat<P>(3, mm * N + a + zero), L[mm], s);
+          s0[a + N * t0 + N2 * t1] = s;
+        }
       }
     }
     __syncthreads();
@@ -481,12 +578,19 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
       double L[N];
 #pragma unroll
       for (int mm = 0; mm < N; ++mm) L[mm] = su[t0 + N * mm + N2 * t1];
+      if constexpr (EO) {
+        double o[N];
+        eo_line<P, 5>(L, o);
 #pragma unroll
-      for (int b = 0; b < N; ++b) {
-        double s = s0[t0 + N * b + N2 * t1];
+        for (int b = 0; b < N; ++b) su[t0 + N * b + N2 * t1] = o[b] + s0[t0 + N * b + N2 * t1];
+      } else {
 #pragma unroll
-        for (int mm = 0; mm < N; ++mm) s = fma(dmat<P>(4, mm * N + b + zero), L[mm], s);
-        su[t0 + N * b + N2 * t1] = s;
+        for (int b = 0; b < N; ++b) {
+          double s = s0[t0 + N * b + N2 * t1];
+#pragma unroll
+          for (int mm = 0; mm < N; ++mm) s = fma(dmat<P>(4, mm * N + b + zero), L[mm], s);
+          su[t0 + N * b + N2 * t1] = s;
+        }
       }
     }
     __syncthreads();
@@ -632,7 +736,7 @@ __global__ void __launch_bounds__(256) k_load(MeshDev m, double* f) {
   constexpr int N = P + 1, N2 = N * N, N3 = N2 * N;
   __shared__ double sD[N * N], sx[N], sw[N];
   for (int t = threadIdx.x; t < N * N; t += blockDim.x) sD[t] = dmat<P>(0, t);
-  for (int t = threadIdx.x; t < N; t += blockDim.x) { sx[t] = c_x[P - 1][t]; sw[t] = c_w[P - 1][t]; }
+  for (int t = threadIdx.x; t < N; t += blockDim.x) { sx[t] = c_xw[0][xOffset(P) + t]; sw[t] = c_xw[1][xOffset(P) + t]; }
   __syncthreads();
   const double pi = 3.14159265358979323846;
   const long long total = m.E * N3;

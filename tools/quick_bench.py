@@ -39,6 +39,10 @@ def main():
         cfgs.append(("config2", inputs.CONFIG2, 1))
     if "3" in which:
         cfgs += [("config3_p%d" % p, inputs.CONFIG3[p], 1) for p in (1, 2, 4, 8, 16)]
+    for w in which:
+        if w.startswith("3:"):
+            p = int(w[2:])
+            cfgs.append(("config3_p%d" % p, inputs.CONFIG3[p], 1))
     if "4" in which:
         cfgs.append(("config4", inputs.CONFIG4, 2))
     for name, d, seed in cfgs:
