@@ -901,8 +901,112 @@ __device__ void cta_apply(const MeshDev& m, const double* __restrict__ G, const 
   __syncthreads();
 }
 
+// Shared-memory variant (N <= kCoarseSmemN): x, r, p, q live in smem (the operator scatter uses
+// shared-memory fp64 atomics), the geometric factors are read through the L1-cached read-only path.
 template <int P>
-__global__ void __launch_bounds__(1024) k_coarse_cg(MeshDev m, const double* __restrict__ G, const double* b,
+__global__ void __launch_bounds__(512) k_coarse_cg_smem(MeshDev m, const double* __restrict__ G,
+                                                        const double* __restrict__ b, double* __restrict__ xout,
+                                                        double* scal, double rtol, int maxit) {
+  constexpr int N = P + 1, N2 = N * N, N3 = N2 * N;
+  using GL = GLayout<P>;
+  extern __shared__ double cg_sm[];
+  __shared__ double red[32];
+  const long long n = m.N;
+  double* x = cg_sm;
+  double* r = x + n;
+  double* p = r + n;
+  double* q = p + n;
+  double rr = 0.0;
+  for (long long g = threadIdx.x; g < n; g += blockDim.x) {
+    const double bg = b[g];
+    x[g] = 0.0; r[g] = bg; p[g] = bg;
+    rr += bg * bg;
+  }
+  rr = block_sum(rr, red);
+  const double bn = sqrt(rr);
+  int it = 0, status = 0;
+  if (bn > 0.0) {
+    for (; it < maxit; ++it) {
+      if (sqrt(rr) <= rtol * bn) break;
+      for (long long g = threadIdx.x; g < n; g += blockDim.x) q[g] = 0.0;
+      __syncthreads();
+      for (long long e = threadIdx.x; e < m.E; e += blockDim.x) {   // q = A_D p on interior rows
+        int ex, ey, ez;
+        elem_coords(m, e, ex, ey, ez);
+        double ue[N3], ve[N3];
+        int gl[N3];
+#pragma unroll
+        for (int c = 0; c < N; ++c)
+#pragma unroll
+          for (int bb = 0; bb < N; ++bb)
+#pragma unroll
+            for (int a = 0; a < N; ++a) {
+              const int l = a + N * (bb + N * c);
+              const int I = ex * P + a, J = ey * P + bb, K = ez * P + c;
+              const bool bnd = I == 0 || I == m.Mx - 1 || J == 0 || J == m.My - 1 || K == 0 || K == m.Mz - 1;
+              const int g = I + m.Mx * (J + m.My * K);
+              gl[l] = bnd ? -1 : g;
+              ue[l] = bnd ? 0.0 : p[g];
+              ve[l] = 0.0;
+            }
+#pragma unroll
+        for (int k = 0; k < N; ++k)
+#pragma unroll
+          for (int j = 0; j < N; ++j)
+#pragma unroll
+            for (int i = 0; i < N; ++i) {
+              double d0 = 0, d1 = 0, d2 = 0;
+#pragma unroll
+              for (int mm = 0; mm < N; ++mm) {
+                d0 = fma(dmat<P>(0, i * N + mm), ue[mm + N * (j + N * k)], d0);
+                d1 = fma(dmat<P>(0, j * N + mm), ue[i + N * (mm + N * k)], d1);
+                d2 = fma(dmat<P>(0, k * N + mm), ue[i + N * (j + N * mm)], d2);
+              }
+              const int ij = i + N * j;
+              const double G00 = __ldg(G + GL::off(e, 0, ij, k)), G01 = __ldg(G + GL::off(e, 1, ij, k));
+              const double G02 = __ldg(G + GL::off(e, 2, ij, k)), G11 = __ldg(G + GL::off(e, 3, ij, k));
+              const double G12 = __ldg(G + GL::off(e, 4, ij, k)), G22 = __ldg(G + GL::off(e, 5, ij, k));
+              const double w0 = G00 * d0 + G01 * d1 + G02 * d2;
+              const double w1 = G01 * d0 + G11 * d1 + G12 * d2;
+              const double w2 = G02 * d0 + G12 * d1 + G22 * d2;
+#pragma unroll
+              for (int mm = 0; mm < N; ++mm) {
+                ve[mm + N * (j + N * k)] = fma(dmat<P>(0, i * N + mm), w0, ve[mm + N * (j + N * k)]);
+                ve[i + N * (mm + N * k)] = fma(dmat<P>(0, j * N + mm), w1, ve[i + N * (mm + N * k)]);
+                ve[i + N * (j + N * mm)] = fma(dmat<P>(0, k * N + mm), w2, ve[i + N * (j + N * mm)]);
+              }
+            }
+#pragma unroll
+        for (int l = 0; l < N3; ++l)
+          if (gl[l] >= 0) atomicAdd(q + gl[l], ve[l]);
+      }
+      __syncthreads();
+      double pq = 0.0;
+      for (long long g = threadIdx.x; g < n; g += blockDim.x) pq += p[g] * q[g];
+      pq = block_sum(pq, red);
+      if (!(pq > 0.0)) { status = 6; break; }
+      const double alpha = rr / pq;
+      double rn = 0.0;
+      for (long long g = threadIdx.x; g < n; g += blockDim.x) {
+        x[g] += alpha * p[g];
+        const double rg = r[g] - alpha * q[g];
+        r[g] = rg;
+        rn += rg * rg;
+      }
+      rn = block_sum(rn, red);
+      const double beta = rn / rr;
+      for (long long g = threadIdx.x; g < n; g += blockDim.x) p[g] = r[g] + beta * p[g];
+      rr = rn;
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+  for (long long g = threadIdx.x; g < n; g += blockDim.x) xout[g] = x[g];
+  if (threadIdx.x == 0) { scal[8] = (double)it; scal[9] = sqrt(rr); scal[10] = (double)status; }
+}
+
+template <int P>
+__global__ void __launch_bounds__(256) k_coarse_cg(MeshDev m, const double* __restrict__ G, const double* b,
                                                     double* x, double* r, double* p, double* q, double* scal,
                                                     double rtol, int maxit) {
   __shared__ double red[32];
@@ -1089,14 +1193,38 @@ cudaError_t launch_export_maps(const MeshDev& m, int32_t* l2g, uint8_t* mask, ui
   return cudaGetLastError();
 }
 
+constexpr int kCoarseThreads = 512;
+constexpr long long kCoarseSmemN = 6400;   // x, r, p, q of up to this many dofs live in shared memory
+
 cudaError_t launch_coarse_cg(const MeshDev& m, const double* G, const double* b, double* x, double* r,
                              double* p, double* q, double* scal, double rtol, int maxit, cudaStream_t s) {
+  if (m.p != 1 && m.p != 2) return cudaErrorInvalidValue;
+  if (m.N <= kCoarseSmemN) {
+    const size_t smem = sizeof(double) * 4 * (size_t)m.N;
+    static bool attr1 = false, attr2 = false;
+    if (m.p == 1) {
+      if (!attr1) {
+        cudaError_t e = cudaFuncSetAttribute(k_coarse_cg_smem<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)(sizeof(double) * 4 * kCoarseSmemN));
+        if (e) return e;
+        attr1 = true;
+      }
+      k_coarse_cg_smem<1><<<1, kCoarseThreads, smem, s>>>(m, G, b, x, scal, rtol, maxit);
+    } else {
+      if (!attr2) {
+        cudaError_t e = cudaFuncSetAttribute(k_coarse_cg_smem<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)(sizeof(double) * 4 * kCoarseSmemN));
+        if (e) return e;
+        attr2 = true;
+      }
+      k_coarse_cg_smem<2><<<1, kCoarseThreads, smem, s>>>(m, G, b, x, scal, rtol, maxit);
+    }
+    return cudaGetLastError();
+  }
   if (m.p == 1)
-    k_coarse_cg<1><<<1, 1024, 0, s>>>(m, G, b, x, r, p, q, scal, rtol, maxit);
-  else if (m.p == 2)
-    k_coarse_cg<2><<<1, 1024, 0, s>>>(m, G, b, x, r, p, q, scal, rtol, maxit);
+    k_coarse_cg<1><<<1, 256, 0, s>>>(m, G, b, x, r, p, q, scal, rtol, maxit);
   else
-    return cudaErrorInvalidValue;
+    k_coarse_cg<2><<<1, 256, 0, s>>>(m, G, b, x, r, p, q, scal, rtol, maxit);
   return cudaGetLastError();
 }
 
