@@ -280,6 +280,13 @@ __global__ void __launch_bounds__(256) k_geometry(MeshDev m, double* __restrict_
 }
 
 // ------------------------------------------------------------------------------------------
+// Programmatic dependent launch (PDL): a kernel launched with programmatic stream serialization
+// may start while its predecessor is still running; griddepcontrol.wait blocks until the
+// predecessor grid has completed and its memory is visible.  Kernels that feed an apply call
+// launch_dependents at their start so the apply can issue its geometric-factor prefetches early.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // TMA / mbarrier / cp.async helpers (inline PTX).
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -357,7 +364,7 @@ struct V4Cfg {
 template <int P, bool DIR, bool GS>
 __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
     k_apply_v4(MeshDev m, const double* __restrict__ G, const double* __restrict__ u, double* __restrict__ v,
-               long long ngroups) {
+               long long ngroups, int wait_mode) {
   using C = V4Cfg<P, GS>;
   constexpr int N = C::N, N2 = C::N2, N3 = C::N3;
   constexpr bool EO = (P % 2 == 0) && P >= 4;   // even-odd line products
@@ -412,10 +419,7 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
   };
 
   long long grp = blockIdx.x;
-  double ru[N];
-  if (grp < ngroups) load_column(grp, ru);
-  if (grp + gstride < ngroups) prefetch_column(grp + gstride);
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0) {   // factor prefetches need nothing from the predecessor kernel
     if (GS) {
       mbar_init(bar, 1);
       if (grp < ngroups) bulk_load(sG, G + grp * C::EPB * 6 * N3, group_bytes(grp), bar);
@@ -424,6 +428,12 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
     }
     if (grp + gstride < ngroups) prefetch_group_l2(grp + gstride);
   }
+  // wait_mode 2: u is produced by the predecessor; 1: only v is (wait before the first scatter)
+  if (wait_mode == 2) pdl_wait();
+  bool waited = (wait_mode != 1);
+  double ru[N];
+  if (grp < ngroups) load_column(grp, ru);
+  if (grp + gstride < ngroups) prefetch_column(grp + gstride);
   unsigned phase = 0;
   for (; grp < ngroups; grp += gstride) {
     constexpr int zero = 0;
@@ -594,6 +604,10 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
       }
     }
     __syncthreads();
+    if (!waited) {
+      pdl_wait();
+      waited = true;
+    }
     if (act) {  // P6: z-line (i=t0, j=t1): v = su + vz, scatter (own column of su)
 #pragma unroll
       for (int c = 0; c < N; ++c) {
@@ -614,10 +628,13 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
 
 template <int P, bool DIR>
 __global__ void __launch_bounds__(128) k_apply_tpe(MeshDev m, const double* __restrict__ G,
-                                                   const double* __restrict__ u, double* __restrict__ v) {
+                                                   const double* __restrict__ u, double* __restrict__ v,
+                                                   int wait_mode) {
   constexpr int N = P + 1, N2 = N * N, N3 = N2 * N;
   using GL = GLayout<P>;
   const long long sxy = (long long)m.Mx * m.My;
+  if (wait_mode == 2) pdl_wait();
+  bool waited = (wait_mode != 1);
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < m.E; e += (long long)gridDim.x * blockDim.x) {
     int ex, ey, ez;
     elem_coords(m, e, ex, ey, ez);
@@ -665,6 +682,10 @@ __global__ void __launch_bounds__(128) k_apply_tpe(MeshDev m, const double* __re
             ve[i + N * (j + N * mm)] = fma(dmat<P>(0, k * N + mm), w2, ve[i + N * (j + N * mm)]);
           }
         }
+    if (!waited) {
+      pdl_wait();
+      waited = true;
+    }
 #pragma unroll
     for (int c = 0; c < N; ++c)
 #pragma unroll
@@ -775,6 +796,7 @@ __global__ void __launch_bounds__(256) k_load(MeshDev m, double* f) {
 // are per row, and each lane writes consecutive doubles of the row.
 __global__ void __launch_bounds__(256) k_init(MeshDev m, int bc, const double* __restrict__ u, double bval,
                                               double* __restrict__ v) {
+  pdl_trigger();
   const int lane = threadIdx.x & 31;
   const long long rows = (long long)m.My * m.Mz;
   const long long wstride = (long long)gridDim.x * (blockDim.x >> 5);
@@ -793,6 +815,7 @@ __global__ void __launch_bounds__(256) k_init(MeshDev m, int bc, const double* _
 __global__ void k_cheb_update(MeshDev m, const double* cur, const double* prev, double* out,
                               const double* __restrict__ b, double* y, const double* __restrict__ dinv,
                               double c1, double c2) {
+  pdl_trigger();
   for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < m.N; g += (long long)gridDim.x * blockDim.x) {
     const double xc = cur[g];
     const double xp = (c1 != 0.0) ? prev[g] : 0.0;
@@ -1089,8 +1112,25 @@ cudaError_t launch_geometry(const MeshDev& m, double* G, int* bad, cudaStream_t 
   return cudaGetLastError();
 }
 
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*k)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t s,
+                              Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, args...);
+}
+
 template <int P, bool DIR>
-static cudaError_t apply_pd(const MeshDev& m, const double* G, const double* u, double* v, cudaStream_t s) {
+static cudaError_t apply_pd(const MeshDev& m, const double* G, const double* u, double* v, int wait_mode,
+                            cudaStream_t s) {
   if constexpr (P <= 2) {
     static int grid = 0;
     if (!grid) {
@@ -1103,8 +1143,7 @@ static cudaError_t apply_pd(const MeshDev& m, const double* G, const double* u, 
     }
     long long blocks = (m.E + 127) / 128;
     if (blocks > grid) blocks = grid;
-    k_apply_tpe<P, DIR><<<(unsigned)blocks, 128, 0, s>>>(m, G, u, v);
-    return cudaSuccess;
+    return launch_pdl(k_apply_tpe<P, DIR>, (unsigned)blocks, 128, 0, s, m, G, u, v, wait_mode);
   } else {
     constexpr bool GS = (P <= 8);
     using C = V4Cfg<P, GS>;
@@ -1123,18 +1162,19 @@ static cudaError_t apply_pd(const MeshDev& m, const double* G, const double* u, 
     const long long groups = (m.E + C::EPB - 1) / C::EPB;
     long long grid = (long long)resident * num_sms;
     if (grid > groups) grid = groups;
-    k_apply_v4<P, DIR, GS><<<(unsigned)grid, C::THREADS, C::SMEM, s>>>(m, G, u, v, groups);
-    return cudaSuccess;
+    return launch_pdl(k_apply_v4<P, DIR, GS>, (unsigned)grid, (unsigned)C::THREADS, C::SMEM, s, m, G, u, v, groups,
+                      wait_mode);
   }
 }
 template <int P>
-static void apply_p(const MeshDev& m, int bc, const double* G, const double* u, double* v, cudaStream_t s,
-                    cudaError_t* err) {
-  *err = (bc == 0) ? apply_pd<P, true>(m, G, u, v, s) : apply_pd<P, false>(m, G, u, v, s);
+static void apply_p(const MeshDev& m, int bc, const double* G, const double* u, double* v, int wait_mode,
+                    cudaStream_t s, cudaError_t* err) {
+  *err = (bc == 0) ? apply_pd<P, true>(m, G, u, v, wait_mode, s) : apply_pd<P, false>(m, G, u, v, wait_mode, s);
 }
-cudaError_t launch_apply(const MeshDev& m, int bc, const double* G, const double* u, double* v, cudaStream_t s) {
+cudaError_t launch_apply(const MeshDev& m, int bc, const double* G, const double* u, double* v, int wait_mode,
+                         cudaStream_t s) {
   cudaError_t err = cudaSuccess;
-  SFMG_DISPATCH_P(m.p, apply_p, m, bc, G, u, v, s, &err);
+  SFMG_DISPATCH_P(m.p, apply_p, m, bc, G, u, v, wait_mode, s, &err);
   if (err) return err;
   return cudaGetLastError();
 }

@@ -122,7 +122,7 @@ static sfmg_status level_build(const sfmg_problem* pr, void* d_ws, size_t ws_byt
 static cudaError_t op_apply(sfmg_level_s* lv, int bc, const double* u, double* v, cudaStream_t s) {
   cudaError_t e = launch_init(lv->m, bc, u, 0.0, v, s);
   if (e) return e;
-  return launch_apply(lv->m, bc, lv->G, u, v, s);
+  return launch_apply(lv->m, bc, lv->G, u, v, 1, s);
 }
 
 // Degree-K Chebyshev application, iterate form of R7:
@@ -149,7 +149,7 @@ static cudaError_t op_cheb(sfmg_level_s* lv, const double* b, double* x, int K, 
     }
     double* out = (k == K - 1) ? A : (k == 0 ? B : prev);
     if (k > 0) {
-      e = launch_apply(lv->m, 0, lv->G, cur, lv->y, s);   // y was re-initialised by the last update
+      e = launch_apply(lv->m, 0, lv->G, cur, lv->y, 2, s);   // y was re-initialised by the last update
       if (e) return e;
     }
     e = launch_cheb_update(lv->m, cur, prev ? prev : cur, out, b, lv->y, lv->dinv, c1, c2, s);
@@ -243,7 +243,7 @@ sfmg_status sfmg_lambda_max(sfmg_level lv, int32_t iters, uint64_t seed, double*
   double* y = lv->y;
   CK(launch_power_start(lv->m, seed, x, y, s));
   for (int it = 0; it < iters; ++it) {
-    CK(launch_apply(lv->m, 0, lv->G, x, y, s));
+    CK(launch_apply(lv->m, 0, lv->G, x, y, 2, s));
     CK(launch_power_step(lv->m, lv->red, x, y, lv->dinv, s));
   }
   CK(cudaMemcpyAsync(h_lambda, lv->red.scalars + 3, sizeof(double), cudaMemcpyDeviceToHost, s));
