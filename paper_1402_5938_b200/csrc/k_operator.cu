@@ -364,7 +364,7 @@ struct V4Cfg {
 template <int P, bool DIR, bool GS>
 __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
     k_apply_v4(MeshDev m, const double* __restrict__ G, const double* __restrict__ u, double* __restrict__ v,
-               long long ngroups, int wait_mode) {
+               long long ngroups, int wait_mode, int write_bnd) {
   using C = V4Cfg<P, GS>;
   constexpr int N = C::N, N2 = C::N2, N3 = C::N3;
   constexpr bool EO = (P % 2 == 0) && P >= 4;   // even-odd line products
@@ -609,11 +609,13 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
       waited = true;
     }
     if (act) {  // P6: z-line (i=t0, j=t1): v = su + vz, scatter (own column of su)
+      const bool own_xy = (t0 > 0 || ex == 0) && (t1 > 0 || ey == 0);
 #pragma unroll
       for (int c = 0; c < N; ++c) {
         bool bnd = false;
         if (DIR) { const int K = ez * P + c; bnd = bxy || K == 0 || K == m.Mz - 1; }
         if (!bnd) atomicAdd(v + gcol + sxy * c, su[t + N2 * c] + vz[c]);
+        else if (write_bnd && own_xy && (c > 0 || ez == 0)) v[gcol + sxy * c] = u[gcol + sxy * c];  // (I-M) u
       }
     }
 #pragma unroll
@@ -629,7 +631,7 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
 template <int P, bool DIR>
 __global__ void __launch_bounds__(128) k_apply_tpe(MeshDev m, const double* __restrict__ G,
                                                    const double* __restrict__ u, double* __restrict__ v,
-                                                   int wait_mode) {
+                                                   int wait_mode, int write_bnd) {
   constexpr int N = P + 1, N2 = N * N, N3 = N2 * N;
   using GL = GLayout<P>;
   const long long sxy = (long long)m.Mx * m.My;
@@ -697,7 +699,9 @@ __global__ void __launch_bounds__(128) k_apply_tpe(MeshDev m, const double* __re
             const int I = ex * P + a, J = ey * P + b, K = ez * P + c;
             bnd = I == 0 || I == m.Mx - 1 || J == 0 || J == m.My - 1 || K == 0 || K == m.Mz - 1;
           }
-          if (!bnd) atomicAdd(v + g0 + a + (long long)m.Mx * b + sxy * c, ve[a + N * (b + N * c)]);
+          const long long g = g0 + a + (long long)m.Mx * b + sxy * c;
+          if (!bnd) atomicAdd(v + g, ve[a + N * (b + N * c)]);
+          else if (write_bnd && (a > 0 || ex == 0) && (b > 0 || ey == 0) && (c > 0 || ez == 0)) v[g] = u[g];
         }
   }
 }
@@ -1130,7 +1134,7 @@ static cudaError_t launch_pdl(void (*k)(KArgs...), unsigned grid, unsigned block
 
 template <int P, bool DIR>
 static cudaError_t apply_pd(const MeshDev& m, const double* G, const double* u, double* v, int wait_mode,
-                            cudaStream_t s) {
+                            int write_bnd, cudaStream_t s) {
   if constexpr (P <= 2) {
     static int grid = 0;
     if (!grid) {
@@ -1143,7 +1147,7 @@ static cudaError_t apply_pd(const MeshDev& m, const double* G, const double* u, 
     }
     long long blocks = (m.E + 127) / 128;
     if (blocks > grid) blocks = grid;
-    return launch_pdl(k_apply_tpe<P, DIR>, (unsigned)blocks, 128, 0, s, m, G, u, v, wait_mode);
+    return launch_pdl(k_apply_tpe<P, DIR>, (unsigned)blocks, 128, 0, s, m, G, u, v, wait_mode, write_bnd);
   } else {
     constexpr bool GS = (P <= 8);
     using C = V4Cfg<P, GS>;
@@ -1163,18 +1167,19 @@ static cudaError_t apply_pd(const MeshDev& m, const double* G, const double* u, 
     long long grid = (long long)resident * num_sms;
     if (grid > groups) grid = groups;
     return launch_pdl(k_apply_v4<P, DIR, GS>, (unsigned)grid, (unsigned)C::THREADS, C::SMEM, s, m, G, u, v, groups,
-                      wait_mode);
+                      wait_mode, write_bnd);
   }
 }
 template <int P>
 static void apply_p(const MeshDev& m, int bc, const double* G, const double* u, double* v, int wait_mode,
-                    cudaStream_t s, cudaError_t* err) {
-  *err = (bc == 0) ? apply_pd<P, true>(m, G, u, v, wait_mode, s) : apply_pd<P, false>(m, G, u, v, wait_mode, s);
+                    int write_bnd, cudaStream_t s, cudaError_t* err) {
+  *err = (bc == 0) ? apply_pd<P, true>(m, G, u, v, wait_mode, write_bnd, s)
+                   : apply_pd<P, false>(m, G, u, v, wait_mode, write_bnd, s);
 }
 cudaError_t launch_apply(const MeshDev& m, int bc, const double* G, const double* u, double* v, int wait_mode,
-                         cudaStream_t s) {
+                         int write_bnd, cudaStream_t s) {
   cudaError_t err = cudaSuccess;
-  SFMG_DISPATCH_P(m.p, apply_p, m, bc, G, u, v, wait_mode, s, &err);
+  SFMG_DISPATCH_P(m.p, apply_p, m, bc, G, u, v, wait_mode, write_bnd, s, &err);
   if (err) return err;
   return cudaGetLastError();
 }

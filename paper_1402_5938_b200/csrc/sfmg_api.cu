@@ -118,11 +118,21 @@ static sfmg_status level_build(const sfmg_problem* pr, void* d_ws, size_t ws_byt
   return SFMG_OK;
 }
 
-// y <- A_D u (bc 0) or A u (bc 1): boundary/zero init then the element kernel
+// y <- A_D u (bc 0) or A u (bc 1).  p <= 2: zero fill, then the thread-per-element kernel whose
+// canonical owner elements also store the boundary pass-through values (I - M) u.  p >= 3: the
+// boundary/zero init kernel, then the persistent kernel launched as its programmatic dependent
+// (its factor prefetches overlap the init).  Both orders were measured; each is the faster for
+// its kernel family.
 static cudaError_t op_apply(sfmg_level_s* lv, int bc, const double* u, double* v, cudaStream_t s) {
-  cudaError_t e = launch_init(lv->m, bc, u, 0.0, v, s);
+  cudaError_t e;
+  if (lv->p <= 2) {
+    e = cudaMemsetAsync(v, 0, sizeof(double) * lv->N, s);
+    if (e) return e;
+    return launch_apply(lv->m, bc, lv->G, u, v, 1, 1, s);
+  }
+  e = launch_init(lv->m, bc, u, 0.0, v, s);
   if (e) return e;
-  return launch_apply(lv->m, bc, lv->G, u, v, 1, s);
+  return launch_apply(lv->m, bc, lv->G, u, v, 1, 0, s);
 }
 
 // Degree-K Chebyshev application, iterate form of R7:
@@ -149,7 +159,7 @@ static cudaError_t op_cheb(sfmg_level_s* lv, const double* b, double* x, int K, 
     }
     double* out = (k == K - 1) ? A : (k == 0 ? B : prev);
     if (k > 0) {
-      e = launch_apply(lv->m, 0, lv->G, cur, lv->y, 2, s);   // y was re-initialised by the last update
+      e = launch_apply(lv->m, 0, lv->G, cur, lv->y, 2, 0, s);   // y was re-initialised by the last update
       if (e) return e;
     }
     e = launch_cheb_update(lv->m, cur, prev ? prev : cur, out, b, lv->y, lv->dinv, c1, c2, s);
@@ -243,7 +253,7 @@ sfmg_status sfmg_lambda_max(sfmg_level lv, int32_t iters, uint64_t seed, double*
   double* y = lv->y;
   CK(launch_power_start(lv->m, seed, x, y, s));
   for (int it = 0; it < iters; ++it) {
-    CK(launch_apply(lv->m, 0, lv->G, x, y, 2, s));
+    CK(launch_apply(lv->m, 0, lv->G, x, y, 2, 0, s));
     CK(launch_power_step(lv->m, lv->red, x, y, lv->dinv, s));
   }
   CK(cudaMemcpyAsync(h_lambda, lv->red.scalars + 3, sizeof(double), cudaMemcpyDeviceToHost, s));

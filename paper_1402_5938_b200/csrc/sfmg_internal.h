@@ -76,9 +76,10 @@ cudaError_t launch_geometry(const MeshDev& m, double* G, int* bad, cudaStream_t 
 cudaError_t launch_init(const MeshDev& m, int bc, const double* u, double bval, double* v, cudaStream_t s);
 // v += A(M u) on interior rows (bc 0) or all rows (bc 1); v must be initialised.  Launched with
 // programmatic dependent launch: wait_mode 1 = only v comes from the preceding kernel (wait before
-// the first scatter), 2 = u does too (wait before the gather).
+// the first scatter), 2 = u does too (wait before the gather).  write_bnd (bc 0): the canonical
+// element of each boundary node stores v = u there, so v only needs to be zero beforehand.
 cudaError_t launch_apply(const MeshDev& m, int bc, const double* G, const double* u, double* v, int wait_mode,
-                         cudaStream_t s);
+                         int write_bnd, cudaStream_t s);
 cudaError_t launch_diag(const MeshDev& m, int bc, const double* G, double* d, cudaStream_t s);
 cudaError_t launch_load(const MeshDev& m, int rhs_id, double* f, cudaStream_t s);
 // out = cur + c1 (cur - prev) + c2 dinv (b - y); then y = bnd ? out : 0 (ready for next apply)
