@@ -141,6 +141,14 @@ sfmg_status sfmg_apply_host(sfmg_level lv, int32_t bc, const double* h_u, double
 sfmg_status sfmg_cheb_host(sfmg_level lv, const double* h_b, double* h_x, int64_t n,
                            int32_t degree, double lam_lo, double lam_hi, void* stream);
 
+/* Benchmark timing of the element (operator) kernel: while enabled, CUDA events are recorded on the
+ * stream around every launch of this level's element kernel (apply and Chebyshev steps).  Recording
+ * events between kernels removes the overlap of that kernel with its predecessor, so enable it only
+ * for a separate measurement pass.  read: accumulated device milliseconds and launch count since the
+ * last reset (syncs). */
+sfmg_status sfmg_profile_enable(sfmg_level lv, int32_t enable);
+sfmg_status sfmg_profile_read(sfmg_level lv, double* ms, int64_t* launches, int32_t reset);
+
 /* ---------------------------------------------------------------- p-transfer */
 /* fine.order == 2 coarse.order on the same element grid, else SFMG_E_PCOARSEN.
  * prolong: d_uf = P0 d_uc with P0 = M_f P M_c, P_gJ = phi^{coarse}_J(xi(g)) (eq. (7)).

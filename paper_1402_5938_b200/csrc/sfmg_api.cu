@@ -4,6 +4,7 @@
 // except the scalar Chebyshev recurrence coefficients (R7).
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -123,16 +124,37 @@ static sfmg_status level_build(const sfmg_problem* pr, void* d_ws, size_t ws_byt
 // boundary/zero init kernel, then the persistent kernel launched as its programmatic dependent
 // (its factor prefetches overlap the init).  Both orders were measured; each is the faster for
 // its kernel family.
+// The element (operator) kernel, with optional event timing for benchmarks (sfmg_profile_*).
+static cudaError_t element_kernel(sfmg_level_s* lv, int bc, const double* u, double* v, int wait_mode,
+                                  int write_bnd, cudaStream_t s) {
+  if (!lv->prof) return launch_apply(lv->m, bc, lv->G, u, v, wait_mode, write_bnd, s);
+  if (lv->prof_used + 2 > lv->prof_ev.size()) {
+    for (int i = 0; i < 64; ++i) {
+      cudaEvent_t ev;
+      cudaError_t e = cudaEventCreate(&ev);
+      if (e) return e;
+      lv->prof_ev.push_back(ev);
+    }
+  }
+  cudaEvent_t a = lv->prof_ev[lv->prof_used], b = lv->prof_ev[lv->prof_used + 1];
+  lv->prof_used += 2;
+  cudaError_t e = cudaEventRecord(a, s);
+  if (e) return e;
+  e = launch_apply(lv->m, bc, lv->G, u, v, wait_mode, write_bnd, s);
+  if (e) return e;
+  return cudaEventRecord(b, s);
+}
+
 static cudaError_t op_apply(sfmg_level_s* lv, int bc, const double* u, double* v, cudaStream_t s) {
   cudaError_t e;
   if (lv->p <= 2) {
     e = cudaMemsetAsync(v, 0, sizeof(double) * lv->N, s);
     if (e) return e;
-    return launch_apply(lv->m, bc, lv->G, u, v, 1, 1, s);
+    return element_kernel(lv, bc, u, v, 1, 1, s);
   }
   e = launch_init(lv->m, bc, u, 0.0, v, s);
   if (e) return e;
-  return launch_apply(lv->m, bc, lv->G, u, v, 1, 0, s);
+  return element_kernel(lv, bc, u, v, 1, 0, s);
 }
 
 // Degree-K Chebyshev application, iterate form of R7:
@@ -159,7 +181,7 @@ static cudaError_t op_cheb(sfmg_level_s* lv, const double* b, double* x, int K, 
     }
     double* out = (k == K - 1) ? A : (k == 0 ? B : prev);
     if (k > 0) {
-      e = launch_apply(lv->m, 0, lv->G, cur, lv->y, 2, 0, s);   // y was re-initialised by the last update
+      e = element_kernel(lv, 0, cur, lv->y, 2, 0, s);   // y was re-initialised by the last update
       if (e) return e;
     }
     e = launch_cheb_update(lv->m, cur, prev ? prev : cur, out, b, lv->y, lv->dinv, c1, c2, s);
@@ -196,10 +218,38 @@ sfmg_status sfmg_level_create(const sfmg_problem* prob, void* d_ws, size_t ws_by
   return level_build(prob, d_ws, ws_bytes, (cudaStream_t)stream, out);
 }
 
+static void free_prof(sfmg_level_s* lv) {
+  for (cudaEvent_t ev : lv->prof_ev) cudaEventDestroy(ev);
+  lv->prof_ev.clear();
+  lv->prof_used = 0;
+}
+
 sfmg_status sfmg_level_destroy(sfmg_level lv) {
   if (!lv) return SFMG_E_ARG;
   if (lv->owned_by_hier) { set_error("level is owned by a hierarchy"); return SFMG_E_ARG; }
+  free_prof(lv);
   delete lv;
+  return SFMG_OK;
+}
+
+sfmg_status sfmg_profile_enable(sfmg_level lv, int32_t enable) {
+  if (!lv) return SFMG_E_ARG;
+  lv->prof = enable != 0;
+  return SFMG_OK;
+}
+
+sfmg_status sfmg_profile_read(sfmg_level lv, double* ms, int64_t* launches, int32_t reset) {
+  if (!lv) return SFMG_E_ARG;
+  double tot = 0.0;
+  for (size_t i = 0; i + 1 < lv->prof_used; i += 2) {
+    CK(cudaEventSynchronize(lv->prof_ev[i + 1]));
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, lv->prof_ev[i], lv->prof_ev[i + 1]));
+    tot += t;
+  }
+  if (ms) *ms = tot;
+  if (launches) *launches = (int64_t)(lv->prof_used / 2);
+  if (reset) lv->prof_used = 0;
   return SFMG_OK;
 }
 
@@ -373,7 +423,12 @@ sfmg_status sfmg_hier_query(const sfmg_problem* fine, const sfmg_mg_params* mg, 
 
 sfmg_status sfmg_hier_destroy(sfmg_hier h) {
   if (!h) return SFMG_E_ARG;
-  for (sfmg_level_s* lv : h->lv) delete lv;
+  for (sfmg_level_s* lv : h->lv) {
+    free_prof(lv);
+    delete lv;
+  }
+  if (h->vc_exec) cudaGraphExecDestroy(h->vc_exec);
+  if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
   delete h;
   return SFMG_OK;
 }
@@ -480,13 +535,56 @@ static cudaError_t vcycle_level(sfmg_hier_s* h, size_t l, const double* b, doubl
   return cudaSuccess;
 }
 
+// The V-cycle is a fixed sequence of ~10^2 small launches (most levels are latency-bound), so it is
+// replayed as a CUDA graph: the first call per (b, x) pair runs eagerly (it also completes every lazy
+// per-kernel setup), the second captures the sequence on a private stream (relaxed mode) and every
+// later call launches the instantiated graph on the caller's stream.  SFMG_NO_GRAPH=1 disables it.
+static cudaError_t vcycle(sfmg_hier_s* h, const double* b, double* x, cudaStream_t s) {
+  static const bool no_graph = getenv("SFMG_NO_GRAPH") && getenv("SFMG_NO_GRAPH")[0] == '1';
+  if (no_graph) return vcycle_level(h, 0, b, x, s);
+  if (h->vc_exec && h->vc_b == b && h->vc_x == x) {
+    h->fine_applies += h->vc_fine_applies;
+    return cudaGraphLaunch(h->vc_exec, s);
+  }
+  if (h->vc_b != b || h->vc_x != x) {
+    h->vc_b = b;
+    h->vc_x = x;
+    h->vc_eager_runs = 0;
+    if (h->vc_exec) {
+      cudaGraphExecDestroy(h->vc_exec);
+      h->vc_exec = nullptr;
+    }
+  }
+  if (h->vc_eager_runs < 1) {
+    ++h->vc_eager_runs;
+    return vcycle_level(h, 0, b, x, s);
+  }
+  cudaError_t e;
+  if (!h->cap_stream && (e = cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking))) return e;
+  // order the capture after the caller's pending work: the graph itself is launched on s below
+  const int64_t fa0 = h->fine_applies;
+  if ((e = cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeRelaxed))) return e;
+  cudaError_t ev = vcycle_level(h, 0, b, x, h->cap_stream);
+  cudaGraph_t graph = nullptr;
+  e = cudaStreamEndCapture(h->cap_stream, &graph);
+  if (ev) { if (graph) cudaGraphDestroy(graph); return ev; }
+  if (e) return e;
+  h->vc_fine_applies = h->fine_applies - fa0;
+  h->fine_applies = fa0;
+  e = cudaGraphInstantiate(&h->vc_exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e) return e;
+  h->fine_applies += h->vc_fine_applies;
+  return cudaGraphLaunch(h->vc_exec, s);
+}
+
 }  // namespace sfmg
 
 extern "C" {
 
 sfmg_status sfmg_vcycle(sfmg_hier h, const double* d_b, double* d_x, void* stream) {
   if (!h || !d_b || !d_x || d_b == d_x) return SFMG_E_ARG;
-  CK(vcycle_level(h, 0, d_b, d_x, (cudaStream_t)stream));
+  CK(vcycle(h, d_b, d_x, (cudaStream_t)stream));
   return SFMG_OK;
 }
 
@@ -516,7 +614,7 @@ sfmg_status sfmg_solve(sfmg_hier h, int32_t mode, const double* d_b, double* d_x
     while (it < max_iter) {
       if (rn <= rtol * r0) { converged = 1; break; }
       if (rn > 10.0 * r0) break;
-      CK(vcycle_level(h, 0, h->pr, h->pz, s));
+      CK(vcycle(h, h->pr, h->pz, s));
       ++vcycles;
       CK(launch_axpy1(d_x, h->pz, N, s));
       CK(op_apply(lv, 0, d_x, h->ph, s));
@@ -533,7 +631,7 @@ sfmg_status sfmg_solve(sfmg_hier h, int32_t mode, const double* d_b, double* d_x
   } else {
     // Algorithm 1 with slots: 12/13 rho_r (alternating), 6 (p,h), 7 |r|^2
     int sa = 12, sb = 13;
-    CK(vcycle_level(h, 0, h->pr, h->pz, s));
+    CK(vcycle(h, h->pr, h->pz, s));
     ++vcycles;
     CK(launch_copy(h->pz, h->pp, N, s));
     CK(launch_dot(lv->red, h->pz, h->pr, N, sa, s));
@@ -550,7 +648,7 @@ sfmg_status sfmg_solve(sfmg_hier h, int32_t mode, const double* d_b, double* d_x
       if (rep && rep->history && it < rep->history_cap) rep->history[it] = rn;
       if (rn <= rtol * r0) { converged = 1; break; }                // convergence test
       if (rn > 10.0 * r0) break;
-      CK(vcycle_level(h, 0, h->pr, h->pz, s));                     // rho = M r
+      CK(vcycle(h, h->pr, h->pz, s));                     // rho = M r
       ++vcycles;
       CK(launch_dot(lv->red, h->pz, h->pr, N, sb, s));             // (rho, r)
       CK(launch_pcg_p(lv->red, h->pp, h->pz, sb, sa, N, s));       // p = rho + beta p

@@ -56,6 +56,10 @@ struct sfmg_level_s {
   int* bad;        // geometry check counter
   size_t ws_bytes;
   bool owned_by_hier;
+  // benchmark timing of the element kernel (sfmg_profile_*): event pairs recorded around launches
+  bool prof = false;
+  std::vector<cudaEvent_t> prof_ev;   // [2 * launches]
+  size_t prof_used = 0;
 };
 
 struct sfmg_hier_s {
@@ -65,6 +69,13 @@ struct sfmg_hier_s {
   std::vector<double*> b, x, r;  // per-level V-cycle vectors
   double *pr, *pz, *pp, *ph;     // PCG vectors on the finest level
   int64_t fine_applies;
+  // V-cycle replayed as a CUDA graph (captured on a private stream, keyed on the b / x pointers)
+  cudaStream_t cap_stream = nullptr;
+  cudaGraphExec_t vc_exec = nullptr;
+  const double* vc_b = nullptr;
+  double* vc_x = nullptr;
+  int64_t vc_fine_applies = 0;
+  int vc_eager_runs = 0;
 };
 
 namespace sfmg {

@@ -72,6 +72,8 @@ _SIG = {
     "sfmg_load_vector": ([_vp, _i32, _vp, _i64, _vp], C.c_int),
     "sfmg_apply_host": ([_vp, _i32, _vp, _vp, _i64, _vp], C.c_int),
     "sfmg_cheb_host": ([_vp, _vp, _vp, _i64, _i32, _d, _d, _vp], C.c_int),
+    "sfmg_profile_enable": ([_vp, _i32], C.c_int),
+    "sfmg_profile_read": ([_vp, _P(_d), _P(_i64), _i32], C.c_int),
     "sfmg_prolong": ([_vp, _vp, _vp, _vp, _vp], C.c_int),
     "sfmg_restrict": ([_vp, _vp, _vp, _vp, _vp], C.c_int),
     "sfmg_hier_query": ([_P(_Problem), _P(_MgParams), _P(C.c_size_t)], C.c_int),
@@ -235,6 +237,14 @@ class Level:
         a = torch.empty((self.E, self.n, 6, self.n ** 2), dtype=torch.float64, device=self.device)
         _ck(_lib.sfmg_export_geometry(self.h, _dptr(a), _stream(stream)), "sfmg_export_geometry")
         return a
+
+    def profile(self, enable=True):
+        _ck(_lib.sfmg_profile_enable(self.h, 1 if enable else 0), "sfmg_profile_enable")
+
+    def profile_read(self, reset=True):
+        ms, n = _d(), _i64()
+        _ck(_lib.sfmg_profile_read(self.h, C.byref(ms), C.byref(n), 1 if reset else 0), "sfmg_profile_read")
+        return ms.value, n.value
 
     # host-buffer (end-to-end) variants; numpy in, numpy out
     def apply_host(self, u: np.ndarray, v: np.ndarray = None, bc=0, stream=None):
