@@ -800,7 +800,6 @@ __global__ void __launch_bounds__(256) k_load(MeshDev m, double* f) {
 // are per row, and each lane writes consecutive doubles of the row.
 __global__ void __launch_bounds__(256) k_init(MeshDev m, int bc, const double* __restrict__ u, double bval,
                                               double* __restrict__ v) {
-  pdl_trigger();
   const int lane = threadIdx.x & 31;
   const long long rows = (long long)m.My * m.Mz;
   const long long wstride = (long long)gridDim.x * (blockDim.x >> 5);
@@ -814,12 +813,12 @@ __global__ void __launch_bounds__(256) k_init(MeshDev m, int bc, const double* _
       vr[I] = b ? (ur ? ur[I] : bval) : 0.0;
     }
   }
+  pdl_trigger();   // after this block's work (see k_cheb_update)
 }
 
 __global__ void k_cheb_update(MeshDev m, const double* cur, const double* prev, double* out,
                               const double* __restrict__ b, double* y, const double* __restrict__ dinv,
                               double c1, double c2) {
-  pdl_trigger();
   for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < m.N; g += (long long)gridDim.x * blockDim.x) {
     const double xc = cur[g];
     const double xp = (c1 != 0.0) ? prev[g] : 0.0;
@@ -827,6 +826,8 @@ __global__ void k_cheb_update(MeshDev m, const double* cur, const double* prev, 
     out[g] = xn;
     y[g] = lattice_boundary(m, g) ? xn : 0.0;
   }
+  pdl_trigger();   // after this block's work: every block of this grid is then resident or done, so
+                   // the dependent persistent apply can never starve it of SM resources
 }
 
 __global__ void k_export_maps(MeshDev m, int32_t* l2g, uint8_t* mask, uint8_t* col) {
