@@ -114,12 +114,14 @@ def test_config5_solves_against_golden(S):
     for mode, name in ((1, "pcg"), (0, "mg_solver")):
         x, rep = H.solve(b, mode=mode, rtol=1e-8, max_iter=200)
         ref = g[name]
-        assert rep["converged"] and ref["converged"]
+        # the oracle's MG-as-solver run with these settings diverges (stops at ||r|| > 10 ||r0||,
+        # S:483); the GPU must reproduce the same outcome and iteration count
+        assert rep["converged"] == ref["converged"], name
         assert abs(rep["iterations"] - ref["iterations"]) <= 1, (name, rep["iterations"], ref["iterations"])
-        assert rep["r_norm"] <= 1e-8 * rep["r0_norm"]
-        # residual histories agree while far above rounding (same algorithm, same arithmetic)
         hg, ho = np.array(rep["history"]), np.array(ref["history"])
         k = min(len(hg), len(ho), 6)
-        np.testing.assert_allclose(hg[:k], ho[:k], rtol=1e-6)
-        xs = x.cpu().numpy()[::99991]
-        np.testing.assert_allclose(xs, ref["x_sample"], rtol=0, atol=1e-6 * np.abs(ref["x_sample"]).max())
+        np.testing.assert_allclose(hg[:k], ho[:k], rtol=1e-6)   # same algorithm, same arithmetic
+        if ref["converged"]:
+            assert rep["r_norm"] <= 1e-8 * rep["r0_norm"]
+            xs = x.cpu().numpy()[::99991]
+            np.testing.assert_allclose(xs, ref["x_sample"], rtol=0, atol=1e-6 * np.abs(ref["x_sample"]).max())
