@@ -262,8 +262,16 @@ def run_gpu(args, rank, world, local_rank):
     k_ms, k_launches = lv.profile_read(reset=True)
     lv.profile(False)
     t_kernel = max_over_ranks(k_ms * 1e-3 / k_launches)
+    traffic = None
+    try:   # dram read + write bytes per launch of this kernel from the committed ncu --set full capture
+        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as fh:
+            tj = json.load(fh)
+        traffic = tj["dram_bytes_read"] + tj["dram_bytes_write"]
+    except Exception:
+        pass
     roof = {"bound": "hbm", "achieved": alg["apply_bytes"] / t_kernel / 1e9, "peak": hbm_peak, "unit": "GB/s",
-            "frac": alg["apply_bytes"] / t_kernel / 1e9 / hbm_peak, "traffic": None,
+            "frac": alg["apply_bytes"] / t_kernel / 1e9 / hbm_peak, "traffic": traffic,
+            "traffic_source": "profiles/r01_traffic.json (ncu --set full, dram__bytes_read.sum + write.sum)",
             "kernel": "k_apply_v4<8,DIR,GS> element kernel (apply + Chebyshev launches; %d launches, %.2f us mean)"
                       % (k_launches, t_kernel * 1e6),
             "peak_kind": peak_kind, "algorithmic_bytes_per_launch": alg["apply_bytes"],
