@@ -107,6 +107,23 @@ def test_random_meshes_apply(S, orc):
         assert rel_err(got, ref, np.abs(ref).max()) <= 1e-11, d
 
 
+@pytest.mark.parametrize("p", [2, 4, 5])
+def test_apply_unaligned_views(S, orc, p):
+    """u and v as 8-byte-offset views (not 16-byte aligned): same result as the oracle."""
+    import torch
+    d = inputs.problem(2, p, ney=3, nez=2, **WARP)
+    g = gpu_level(S, d)
+    o = orc_level(orc, d, tier=3, geom_tier=3)
+    u = inputs.uniform_pm1(5, o.N)
+    ref = o.apply(u, 0, tier=3)
+    ub = torch.zeros(o.N + 1, dtype=torch.float64, device="cuda")
+    vb = torch.full((o.N + 1,), 7.0, dtype=torch.float64, device="cuda")
+    ub[1:] = to_gpu(u)
+    g.apply(ub[1:], vb[1:])
+    assert float(vb[0]) == 7.0
+    assert rel_err(vb[1:].cpu().numpy(), ref, np.abs(ref).max()) <= 1e-11
+
+
 def test_config1_full_workload(S, orc):
     """Config 1: 4^3 affine, p=4, mu = 1; A u from seed 0, then a degree-3 Chebyshev application
     (b = 0, x0 = u, R16) on [0.1, 1.1] lambda_max with 10 power iterations (seed 12345)."""
