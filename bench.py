@@ -103,6 +103,19 @@ class ClockSampler:
                 "samples": len(rows), "reasons": reasons}
 
 
+def fp64_peak():
+    """FP64 vector (DFMA) peak measured on this GPU by tools/fp64_peak; None if unavailable."""
+    exe = os.path.join(ROOT, "tools", "fp64_peak")
+    try:
+        if not os.path.exists(exe):
+            from paper_1402_5938_b200 import _build
+            _build.build_tools()
+        out = subprocess.run([exe], capture_output=True, text=True, timeout=120).stdout.strip().splitlines()
+        return json.loads(out[-1])
+    except Exception as ex:  # measurement tool only; the bench line does not depend on it
+        return {"error": str(ex)[:200]}
+
+
 # ------------------------------------------------------------------------------------------ multi-rank
 def reduce_max(x: float, world: int, device) -> float:
     """Max over ranks of a per-rank time (the contract's max-over-ranks timing); identity at N=1."""
@@ -313,6 +326,12 @@ def run_gpu(args, rank, world, local_rank):
     if rank == 0 and world == 1 and not args.no_cpu:
         gd, cores, sample = oracle_apply_sample(d, inputs.SEEDS[2])
         out["cpu_baseline"] = {"value": gd, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample}
+        if not args.quick:   # the oracle also at T=1
+            import oracle
+            oracle.set_threads(1)
+            g1, c1, s1 = oracle_apply_sample(d, inputs.SEEDS[2], target_s=4.0)
+            oracle.set_threads(cores)
+            out["cpu_baseline_t1"] = {"value": g1, "unit": UNIT, "cores": c1, "kind": "oracle", "sample": s1}
     if rank == 0:
         print(json.dumps(out), flush=True)
 
@@ -324,7 +343,8 @@ def time_events(fn, stream, flush, reps, warm=3):
     torch.cuda.synchronize()
     ts = []
     for k in range(reps):
-        flush.fill_(float(k))
+        if flush is not None:
+            flush.fill_(float(k))
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
         fn()
@@ -337,6 +357,9 @@ def time_events(fn, stream, flush, reps, warm=3):
 def run_extras(args, sfmg, dev, stream, flush, hbm_peak):
     import torch
     out = {}
+    pk = fp64_peak()
+    out["fp64_peak"] = pk
+    fp64_tf = pk.get("fp64_dfma_tflops") if isinstance(pk, dict) else None
     sweep = []
     for p in (1, 2, 4, 8, 16):
         d = inputs.CONFIG3[p]
@@ -346,10 +369,13 @@ def run_extras(args, sfmg, dev, stream, flush, hbm_peak):
         v, b, x = torch.empty_like(u), torch.zeros_like(u), u.clone()
         lam = lv.lambda_max(10, inputs.POWER_SEED)
         ta = time_events(lambda: lv.apply(u, v), stream, flush, 20)
+        tw = time_events(lambda: lv.apply(u, v), stream, None, 20)
         tc = time_events(lambda: lv.cheb(b, x, 4, 0.1 * lam, 1.1 * lam), stream, flush, 10) / 4
         sweep.append({"p": p, "ne": d["nex"], "apply_us": ta * 1e6, "apply_gdofs": lv.N / ta / 1e9,
                       "apply_hbm_frac": alg["apply_bytes"] / ta / 1e9 / hbm_peak,
                       "apply_tflops": alg["apply_flops"] / ta / 1e12,
+                      "apply_fp64_frac": (alg["apply_flops"] / ta / 1e12 / fp64_tf) if fp64_tf else None,
+                      "apply_warm_us": tw * 1e6, "apply_warm_gdofs": lv.N / tw / 1e9,
                       "cheb_step_us": tc * 1e6, "cheb_step_gdofs": lv.N / tc / 1e9,
                       "cheb_step_hbm_frac": alg["step_bytes"] / tc / 1e9 / hbm_peak})
         del lv, u, v, b, x

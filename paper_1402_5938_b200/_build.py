@@ -56,5 +56,14 @@ def build(force: bool = False) -> str:
     return LIB
 
 
+def build_tools() -> str:
+    """Measurement tools (not the library): tools/fp64_peak, the DFMA-chain FP64 peak benchmark."""
+    src = os.path.join(ROOT, "tools", "fp64_peak.cu")
+    exe = os.path.join(ROOT, "tools", "fp64_peak")
+    if _stale(exe, [src]):
+        subprocess.check_call([NVCC, *ARCH, "-O3", "-o", exe, src])
+    return exe
+
+
 if __name__ == "__main__":
     print(build())
