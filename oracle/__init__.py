@@ -74,6 +74,13 @@ def lib():
         L.orc_lambda_max.argtypes = [vp, i, u64]
         L.orc_lambda_max.restype = d
         L.orc_cheb.argtypes = [vp, vp, vp, i, d, d]
+        L.orc_lambda_arnoldi.argtypes = [vp, i, u64]
+        L.orc_lambda_arnoldi.restype = d
+        L.orc_jacobi.argtypes = [vp, vp, vp, i, d]
+        L.orc_pair_kind.argtypes = [vp, vp]
+        L.orc_hier_create2.restype = vp
+        L.orc_hier_create2.argtypes = [i, i, i, i, i, d, i, d, d, i, i, i, d, d, i, u64, d, i, i, i,
+                                       i, d, i, i, C.POINTER(C.c_int)]
         L.orc_prolong.argtypes = [vp, vp, vp, vp]
         L.orc_restrict.argtypes = [vp, vp, vp, vp]
         L.orc_load_vector.argtypes = [vp, i, vp]
@@ -257,6 +264,16 @@ class Level:
     def lambda_max(self, iters=10, seed=12345):
         return float(lib().orc_lambda_max(self.h, iters, seed))
 
+    def lambda_arnoldi(self, m=10, seed=12345):
+        """lambda_max(D^-1 A_D) from m Arnoldi iterations in the D-inner product (R26)."""
+        return float(lib().orc_lambda_arnoldi(self.h, m, seed))
+
+    def jacobi(self, b, x, steps, omega=2.0 / 3.0):
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        x = np.array(x, dtype=np.float64, copy=True)
+        lib().orc_jacobi(self.h, _p(b), _p(x), steps, omega)
+        return x
+
     def cheb(self, b, x, degree, lo, hi):
         b = np.ascontiguousarray(b, dtype=np.float64)
         x = np.array(x, dtype=np.float64, copy=True)
@@ -280,7 +297,7 @@ def prolong(coarse: Level, fine: Level, uc):
     uf = np.zeros(fine.N)
     rc = lib().orc_prolong(coarse.h, fine.h, _p(uc), _p(uf))
     if rc:
-        raise ValueError("levels are not p and p/2 on one grid")
+        raise ValueError("levels are neither (p/2, p) on one grid nor (ne/2, ne) at one order")
     return uf
 
 
@@ -289,7 +306,7 @@ def restrict(coarse: Level, fine: Level, rf):
     rc_ = np.zeros(coarse.N)
     rc = lib().orc_restrict(coarse.h, fine.h, _p(rf), _p(rc_))
     if rc:
-        raise ValueError("levels are not p and p/2 on one grid")
+        raise ValueError("levels are neither (p/2, p) on one grid nor (ne/2, ne) at one order")
     return rc_
 
 
@@ -314,19 +331,33 @@ class _LevelView(Level):
 
 
 class Hier:
+    """p-multigrid hierarchy p, p/2, ..., 1 (+ h_levels geometric coarsenings of the p = 1 mesh).
+    smoother 0: Chebyshev-Jacobi of `degree`; 1: damped point Jacobi (omega), one step per smoothing
+    application.  lambda_method 0: power iteration (R9); 1: Arnoldi (R26)."""
+
     def __init__(self, nex, ney, nez, p, warp=0, amp=0.0, coeff=0, c0=1.0, c1=0.0,
                  nu_pre=2, nu_post=2, degree=4, lo_frac=0.1, hi_frac=1.1, power_iters=10,
-                 seed=12345, coarse_rtol=1e-10, coarse_maxit=10000, geom_tier=3, tier=3):
+                 seed=12345, coarse_rtol=1e-10, coarse_maxit=10000, geom_tier=3, tier=3,
+                 smoother=0, omega=2.0 / 3.0, lambda_method=0, h_levels=0):
         st = C.c_int(0)
-        self.h = lib().orc_hier_create(nex, ney, nez, p, warp, amp, coeff, c0, c1, nu_pre, nu_post,
-                                       degree, lo_frac, hi_frac, power_iters, seed, coarse_rtol,
-                                       coarse_maxit, geom_tier, tier, C.byref(st))
+        self.h = lib().orc_hier_create2(nex, ney, nez, p, warp, amp, coeff, c0, c1, nu_pre, nu_post,
+                                        degree, lo_frac, hi_frac, power_iters, seed, coarse_rtol,
+                                        coarse_maxit, geom_tier, tier, smoother, omega, lambda_method,
+                                        h_levels, C.byref(st))
         self.status = st.value
         if not self.h:
             raise ValueError("cannot build hierarchy (status %d)" % st.value)
         self.nlevels = int(lib().orc_hier_nlevels(self.h))
         self.levels = [_LevelView(lib().orc_hier_level(self.h, l), self) for l in range(self.nlevels)]
-        for lv, q in zip(self.levels, [p >> l for l in range(self.nlevels)]):
+        orders = []
+        q = p
+        while True:
+            orders.append(q)
+            if q == 1:
+                break
+            q //= 2
+        orders += [1] * h_levels
+        for lv, q in zip(self.levels, orders):
             lv.p = q
             lv.n = q + 1
         self.N = self.levels[0].N

@@ -585,6 +585,175 @@ void restrict_(const Level& C, const Level& F, const double* rf, double* rc) {
   for (int64_t g = 0; g < C.N; ++g) if (C.boundary(g)) rc[g] = 0.0;
 }
 
+/* ------------------------------------------------------------------ h-transfer */
+
+// Position of fine lattice coordinate I (one axis) in the coarse element grid: the reference-cube
+// coordinate X = (e_f + (xhat^F_i + 1)/2) / ne_f of the fine node, the canonical (lowest-index)
+// coarse element e_c containing it and the local coordinate xi in [-1, 1] (R25: the element grids
+// are nested in reference-lattice coordinates).
+inline void h_position(int64_t I, int pf, const std::vector<double>& xf, int nef, int nec, int& ec, double& xi) {
+  int ef, i;
+  owner_1d(I, pf, ef, i);
+  const double X = (ef + 0.5 * (xf[i] + 1.0)) / nef;
+  const double t = X * nec;
+  double fl = std::floor(t);
+  ec = (int)fl;
+  if (t == fl && ec > 0) ec -= 1;   // on a coarse element face: the lower element
+  if (ec >= nec) ec = nec - 1;
+  xi = 2.0 * (t - ec) - 1.0;
+}
+
+// eq. (7) across meshes: P_gJ = phi^C_J(X(g)), C and F of the same order with F.ne = 2 C.ne; P0 =
+// M_f P M_c (R12).  Direct definition, one fine node at a time.
+void prolong_h(const Level& C, const Level& F, const double* uc, double* uf) {
+  const int nc = C.n;
+#pragma omp parallel for schedule(static)
+  for (int64_t g = 0; g < F.N; ++g) {
+    if (F.boundary(g)) { uf[g] = 0.0; continue; }
+    int64_t IX = g % F.Mx, JY = (g / F.Mx) % F.My, KZ = g / (F.Mx * F.My);
+    int ex, ey, ez;
+    double xi, eta, zeta;
+    h_position(IX, F.p, F.B.x, F.nex, C.nex, ex, xi);
+    h_position(JY, F.p, F.B.x, F.ney, C.ney, ey, eta);
+    h_position(KZ, F.p, F.B.x, F.nez, C.nez, ez, zeta);
+    int64_t e = ex + (int64_t)C.nex * (ey + (int64_t)C.ney * ez);
+    double s = 0.0;
+    for (int c = 0; c < nc; ++c) for (int b = 0; b < nc; ++b) for (int a = 0; a < nc; ++a) {
+      int64_t gc = C.l2g(e, a, b, c);
+      if (C.boundary(gc)) continue;
+      s += lagrange(C.B.x, a, xi) * lagrange(C.B.x, b, eta) * lagrange(C.B.x, c, zeta) * uc[gc];
+    }
+    uf[g] = s;
+  }
+}
+
+// R = P0^T for the h pair: every interior fine node adds P_gJ r_g to the interior coarse nodes J
+// of its canonical coarse element (sequential: the h-levels are small).
+void restrict_h(const Level& C, const Level& F, const double* rf, double* rc) {
+  const int nc = C.n;
+  for (int64_t g = 0; g < C.N; ++g) rc[g] = 0.0;
+  for (int64_t g = 0; g < F.N; ++g) {
+    if (F.boundary(g)) continue;
+    int64_t IX = g % F.Mx, JY = (g / F.Mx) % F.My, KZ = g / (F.Mx * F.My);
+    int ex, ey, ez;
+    double xi, eta, zeta;
+    h_position(IX, F.p, F.B.x, F.nex, C.nex, ex, xi);
+    h_position(JY, F.p, F.B.x, F.ney, C.ney, ey, eta);
+    h_position(KZ, F.p, F.B.x, F.nez, C.nez, ez, zeta);
+    int64_t e = ex + (int64_t)C.nex * (ey + (int64_t)C.ney * ez);
+    for (int c = 0; c < nc; ++c) for (int b = 0; b < nc; ++b) for (int a = 0; a < nc; ++a) {
+      int64_t gc = C.l2g(e, a, b, c);
+      if (C.boundary(gc)) continue;
+      rc[gc] += lagrange(C.B.x, a, xi) * lagrange(C.B.x, b, eta) * lagrange(C.B.x, c, zeta) * rf[g];
+    }
+  }
+}
+
+// Level pair kind: 1 = p pair (F.p = 2 C.p, same mesh), 2 = h pair (same p, F.ne = 2 C.ne), 0 = neither.
+int pair_kind(const Level& C, const Level& F) {
+  const bool same_mesh = C.nex == F.nex && C.ney == F.ney && C.nez == F.nez;
+  if (same_mesh && F.p == 2 * C.p) return 1;
+  if (C.p == F.p && F.nex == 2 * C.nex && F.ney == 2 * C.ney && F.nez == 2 * C.nez) return 2;
+  return 0;
+}
+void transfer_prolong(const Level& C, const Level& F, const double* uc, double* uf) {
+  if (pair_kind(C, F) == 2) prolong_h(C, F, uc, uf); else prolong(C, F, uc, uf);
+}
+void transfer_restrict(const Level& C, const Level& F, const double* rf, double* rc) {
+  if (pair_kind(C, F) == 2) restrict_h(C, F, rf, rc); else restrict_(C, F, rf, rc);
+}
+
+/* ------------------------------------------------------------------ NEXT-1 smoother / estimator */
+
+// Damped point Jacobi, omega = 2/3 in the paper:
+// x <- x + omega D^{-1} (b - A_D x); one apply per step.
+void jacobi(Level& L, const double* b, double* x, int steps, double omega, int64_t* applies) {
+  const std::vector<double>& d = level_diag(L);
+  std::vector<double> Ax(L.N);
+  for (int s = 0; s < steps; ++s) {
+    apply(L, 0, x, Ax.data(), L.tier);
+    if (applies) ++*applies;
+    for (int64_t g = 0; g < L.N; ++g) x[g] += omega * (b[g] - Ax[g]) / d[g];
+  }
+}
+
+// Eigenvalues of a small symmetric matrix (row-major, n x n) by cyclic Jacobi rotations.
+void sym_eig_jacobi(int n, std::vector<double> A, std::vector<double>& ev) {
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    double off = 0.0;
+    for (int i = 0; i < n; ++i) for (int j = 0; j < n; ++j) if (i != j) off += A[i * n + j] * A[i * n + j];
+    if (off < 1e-30) break;
+    for (int pp = 0; pp < n - 1; ++pp)
+      for (int q = pp + 1; q < n; ++q) {
+        double apq = A[pp * n + q];
+        if (apq == 0.0) continue;
+        double theta = (A[q * n + q] - A[pp * n + pp]) / (2.0 * apq);
+        double t = (theta >= 0 ? 1.0 : -1.0) / (std::fabs(theta) + std::sqrt(theta * theta + 1.0));
+        double c = 1.0 / std::sqrt(t * t + 1.0), sn = t * c;
+        for (int k = 0; k < n; ++k) {   // A <- J^T A J
+          double akp = A[k * n + pp], akq = A[k * n + q];
+          A[k * n + pp] = c * akp - sn * akq;
+          A[k * n + q] = sn * akp + c * akq;
+        }
+        for (int k = 0; k < n; ++k) {
+          double apk = A[pp * n + k], aqk = A[q * n + k];
+          A[pp * n + k] = c * apk - sn * aqk;
+          A[q * n + k] = sn * apk + c * aqk;
+        }
+      }
+  }
+  ev.resize(n);
+  for (int i = 0; i < n; ++i) ev[i] = A[i * n + i];
+}
+
+// lambda_max(D^{-1} A_D) from m Arnoldi iterations (reading R26): Arnoldi with
+// modified Gram-Schmidt in the D-inner product <x, y>_D = sum d x y, in which D^{-1}A_D is
+// self-adjoint; start = splitmix64(seed) uniform in [-1,1] with the boundary zeroed (R9).  The
+// estimate is the largest eigenvalue of the k x k Hessenberg matrix H (k = m, or fewer on an
+// invariant subspace), symmetric tridiagonal up to rounding; its symmetric part is diagonalised.
+double lambda_arnoldi(Level& L, int m, uint64_t seed, int64_t* applies) {
+  const std::vector<double>& d = level_diag(L);
+  const int64_t N = L.N;
+  auto dotD = [&](const std::vector<double>& a, const std::vector<double>& b) {
+    double s = 0.0;
+    for (int64_t g = 0; g < N; ++g) s += d[g] * a[g] * b[g];
+    return s;
+  };
+  std::vector<std::vector<double>> V;
+  std::vector<double> v(N), w(N), Aw(N);
+  for (int64_t g = 0; g < N; ++g) v[g] = L.boundary(g) ? 0.0 : uniform_pm1(seed, (uint64_t)g);
+  double nv = std::sqrt(dotD(v, v));
+  for (int64_t g = 0; g < N; ++g) v[g] /= nv;
+  V.push_back(v);
+  std::vector<double> H((m + 1) * m, 0.0);   // H[i*m + j]
+  int k = 0;
+  for (int j = 0; j < m; ++j) {
+    apply(L, 0, V[j].data(), Aw.data(), L.tier);
+    if (applies) ++*applies;
+    for (int64_t g = 0; g < N; ++g) w[g] = Aw[g] / d[g];
+    const double wn0 = std::sqrt(dotD(w, w));
+    for (int pass = 0; pass < 2; ++pass)   // modified Gram-Schmidt, repeated once ("twice is enough")
+      for (int i = 0; i <= j; ++i) {
+        double h = dotD(w, V[i]);
+        H[i * m + j] += h;
+        for (int64_t g = 0; g < N; ++g) w[g] -= h * V[i][g];
+      }
+    k = j + 1;
+    double hn = std::sqrt(dotD(w, w));
+    H[(j + 1) * m + j] = hn;
+    if (hn <= 1e-10 * wn0) break;   // invariant subspace reached (Krylov space exhausted)
+    for (int64_t g = 0; g < N; ++g) w[g] /= hn;
+    V.push_back(w);
+  }
+  std::vector<double> S(k * k), ev;
+  for (int i = 0; i < k; ++i)
+    for (int j = 0; j < k; ++j) S[i * k + j] = 0.5 * (H[i * m + j] + H[j * m + i]);
+  sym_eig_jacobi(k, S, ev);
+  double lam = ev[0];
+  for (double e : ev) lam = std::max(lam, e);
+  return lam;
+}
+
 /* ------------------------------------------------------------------ hierarchy / solvers */
 
 struct Hier {
@@ -594,6 +763,9 @@ struct Hier {
   double lo_frac, hi_frac, coarse_rtol;
   int coarse_maxit, power_iters;
   uint64_t seed;
+  int smoother = 0;          // 0 Chebyshev-Jacobi (degree K), 1 damped point Jacobi (omega)
+  double omega = 2.0 / 3.0;
+  int lambda_method = 0;     // 0 power iteration (R9), 1 Arnoldi (R26)
   int64_t fine_applies = 0;
   int64_t coarse_iters_last = 0;
 };
@@ -635,19 +807,24 @@ int vcycle(Hier& H, int l, const double* b, double* x) {
   if (l == (int)H.lv.size() - 1) return coarse_cg(H, b, x);
   for (int64_t g = 0; g < N; ++g) x[g] = 0.0;
   double lo = H.lo_frac * H.lam[l], hi = H.hi_frac * H.lam[l];
-  for (int s = 0; s < H.nu_pre; ++s) chebyshev(L, b, x, H.K, lo, hi, counter_for(H, l));
+  // one smoothing application: a degree-K Chebyshev polynomial, or one damped Jacobi step
+  auto smooth = [&]() {
+    if (H.smoother == 1) jacobi(L, b, x, 1, H.omega, counter_for(H, l));
+    else chebyshev(L, b, x, H.K, lo, hi, counter_for(H, l));
+  };
+  for (int s = 0; s < H.nu_pre; ++s) smooth();
   std::vector<double> r(N);
   apply(L, 0, x, r.data(), L.tier);
   if (int64_t* c = counter_for(H, l)) ++*c;
   for (int64_t g = 0; g < N; ++g) r[g] = b[g] - r[g];
   Level& C = *H.lv[l + 1];
   std::vector<double> bc(C.N), ec(C.N), ef(N);
-  restrict_(C, L, r.data(), bc.data());
+  transfer_restrict(C, L, r.data(), bc.data());
   int st = vcycle(H, l + 1, bc.data(), ec.data());
   if (st) return st;
-  prolong(C, L, ec.data(), ef.data());
+  transfer_prolong(C, L, ec.data(), ef.data());
   for (int64_t g = 0; g < N; ++g) x[g] += ef[g];
-  for (int s = 0; s < H.nu_post; ++s) chebyshev(L, b, x, H.K, lo, hi, counter_for(H, l));
+  for (int s = 0; s < H.nu_post; ++s) smooth();
   return 0;
 }
 
@@ -974,17 +1151,28 @@ int orc_cheb(void* h, const double* b, double* x, int K, double lo, double hi) {
   return 0;
 }
 
+double orc_lambda_arnoldi(void* h, int m, uint64_t seed) {
+  return lambda_arnoldi(*(Level*)h, m, seed, nullptr);
+}
+
+int orc_jacobi(void* h, const double* b, double* x, int steps, double omega) {
+  jacobi(*(Level*)h, b, x, steps, omega, nullptr);
+  return 0;
+}
+
+int orc_pair_kind(void* hc, void* hf) { return pair_kind(*(Level*)hc, *(Level*)hf); }
+
 int orc_prolong(void* hc, void* hf, const double* uc, double* uf) {
   Level* C = (Level*)hc; Level* F = (Level*)hf;
-  if (F->p != 2 * C->p || F->nex != C->nex || F->ney != C->ney || F->nez != C->nez) return 5;
-  prolong(*C, *F, uc, uf);
+  if (!pair_kind(*C, *F)) return 5;   // p pair or h pair
+  transfer_prolong(*C, *F, uc, uf);
   return 0;
 }
 
 int orc_restrict(void* hc, void* hf, const double* rf, double* rc) {
   Level* C = (Level*)hc; Level* F = (Level*)hf;
-  if (F->p != 2 * C->p || F->nex != C->nex || F->ney != C->ney || F->nez != C->nez) return 5;
-  restrict_(*C, *F, rf, rc);
+  if (!pair_kind(*C, *F)) return 5;
+  transfer_restrict(*C, *F, rf, rc);
   return 0;
 }
 
@@ -1062,17 +1250,24 @@ int orc_cg_dense(int n, const double* A, const double* b, double* x, double rtol
   return 0;
 }
 
-// p-multigrid hierarchy p, p/2, ..., 1 on one element grid (R20).
-void* orc_hier_create(int nex, int ney, int nez, int p, int warp, double amp, int coeff, double c0,
-                      double c1, int nu_pre, int nu_post, int K, double lo_frac, double hi_frac,
-                      int power_iters, uint64_t seed, double coarse_rtol, int coarse_maxit,
-                      int geom_tier, int tier, int* status) {
+// p-multigrid hierarchy p, p/2, ..., 1 on one element grid (R20), followed by h_levels
+// geometric coarsenings of the p = 1 mesh (ne -> ne/2 -> ...; NEXT-1).
+// smoother 0: Chebyshev-Jacobi of degree K; 1: damped point Jacobi (omega), one step per smoothing
+// application.  lambda_method 0: power iteration (R9), 1: Arnoldi (R26), power_iters steps.
+void* orc_hier_create2(int nex, int ney, int nez, int p, int warp, double amp, int coeff, double c0,
+                       double c1, int nu_pre, int nu_post, int K, double lo_frac, double hi_frac,
+                       int power_iters, uint64_t seed, double coarse_rtol, int coarse_maxit,
+                       int geom_tier, int tier, int smoother, double omega, int lambda_method, int h_levels,
+                       int* status) {
   *status = 0;
   for (int q = p; q > 1; q /= 2)
     if (q % 2) { *status = 5; return nullptr; }
+  for (int j = 0; j < h_levels; ++j)
+    if (((nex >> j) % 2) || ((ney >> j) % 2) || ((nez >> j) % 2)) { *status = 5; return nullptr; }
   Hier* H = new Hier();
   H->nu_pre = nu_pre; H->nu_post = nu_post; H->K = K; H->lo_frac = lo_frac; H->hi_frac = hi_frac;
   H->power_iters = power_iters; H->seed = seed; H->coarse_rtol = coarse_rtol; H->coarse_maxit = coarse_maxit;
+  H->smoother = smoother; H->omega = omega; H->lambda_method = lambda_method;
   for (int q = p; q >= 1; q /= 2) {
     Level* L = (Level*)orc_level_create(nex, ney, nez, q, warp, amp, coeff, c0, c1, 1, geom_tier, tier);
     if (!L) { *status = 1; return H; }
@@ -1080,9 +1275,26 @@ void* orc_hier_create(int nex, int ney, int nez, int p, int warp, double amp, in
     H->lv.push_back(L);
     if (q == 1) break;
   }
+  for (int j = 1; j <= h_levels; ++j) {
+    Level* L = (Level*)orc_level_create(nex >> j, ney >> j, nez >> j, 1, warp, amp, coeff, c0, c1, 1, geom_tier, tier);
+    if (!L) { *status = 1; return H; }
+    if (L->status) *status = L->status;
+    H->lv.push_back(L);
+  }
   H->lam.assign(H->lv.size(), 0.0);
-  for (size_t l = 0; l + 1 < H->lv.size(); ++l) H->lam[l] = lambda_max(*H->lv[l], power_iters, seed, nullptr);
+  for (size_t l = 0; l + 1 < H->lv.size(); ++l)
+    H->lam[l] = lambda_method == 1 ? lambda_arnoldi(*H->lv[l], power_iters, seed, nullptr)
+                                   : lambda_max(*H->lv[l], power_iters, seed, nullptr);
   return H;
+}
+
+void* orc_hier_create(int nex, int ney, int nez, int p, int warp, double amp, int coeff, double c0,
+                      double c1, int nu_pre, int nu_post, int K, double lo_frac, double hi_frac,
+                      int power_iters, uint64_t seed, double coarse_rtol, int coarse_maxit,
+                      int geom_tier, int tier, int* status) {
+  return orc_hier_create2(nex, ney, nez, p, warp, amp, coeff, c0, c1, nu_pre, nu_post, K, lo_frac, hi_frac,
+                          power_iters, seed, coarse_rtol, coarse_maxit, geom_tier, tier, 0, 2.0 / 3.0, 0, 0,
+                          status);
 }
 
 void orc_hier_destroy(void* h) {
