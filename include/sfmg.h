@@ -60,9 +60,11 @@ typedef struct {
   double c0, c1;           /*   3: c0 + c1 sum_i cos^2(2 pi x_i); S = sin2pix sin2piy sin2piz */
 } sfmg_problem;
 
-/* p-multigrid parameters (R7-R11, R13). */
+/* p-multigrid parameters (R7-R11, R13).  The last four fields select
+ * the paper's own settings: zero-initialise the struct, or use the Python
+ * MgParams defaults, to get the BASELINE configuration (Chebyshev, power iteration, no h levels). */
 typedef struct {
-  int32_t nu_pre, nu_post;   /* Chebyshev applications before / after the coarse correction */
+  int32_t nu_pre, nu_post;   /* smoothing applications before / after the coarse correction */
   int32_t cheb_degree;       /* K: steps (= applies) per Chebyshev application               */
   double eig_lo_frac;        /* interval [lo_frac lambda, hi_frac lambda]; BASELINE 0.1, 1.1  */
   double eig_hi_frac;
@@ -70,6 +72,15 @@ typedef struct {
   uint64_t power_seed;       /* splitmix64 seed of the power-iteration start vector; 12345   */
   double coarse_rtol;        /* p = 1 coarse CG: ||r|| <= coarse_rtol ||b||; 1e-10           */
   int32_t coarse_max_iter;   /* 10000                                                        */
+  int32_t smoother;          /* 0: one smoothing application = a degree-cheb_degree Chebyshev- */
+                             /*    Jacobi polynomial; 1: one damped point-Jacobi step         */
+                             /*    x += jacobi_omega D^{-1} (b - A_D x)  */
+  double jacobi_omega;       /* 2/3 in the paper; (0, 2)                                       */
+  int32_t lambda_method;     /* 0: power_iters power iterations (R9); 1: power_iters Arnoldi    */
+                             /*    steps in the D-inner product (R26)     */
+  int32_t h_levels;          /* geometric coarsenings of the p = 1 mesh after p-coarsening     */
+                             /*    (ne -> ne/2, trilinear h-transfer); */
+                             /*    every ne must be divisible by 2^h_levels                   */
 } sfmg_mg_params;
 
 /* Solve report.  history: caller-owned host buffer of history_cap doubles
@@ -85,7 +96,8 @@ typedef struct {
 } sfmg_report;
 
 typedef struct sfmg_level_s* sfmg_level; /* one (mesh, p): G, diag, scratch                    */
-typedef struct sfmg_hier_s* sfmg_hier;   /* levels p, p/2, ..., 1 on one element grid          */
+typedef struct sfmg_hier_s* sfmg_hier;   /* levels p, p/2, ..., 1 on one element grid, then     */
+                                         /* h_levels coarsenings of the p = 1 mesh            */
 
 const char* sfmg_version(void);
 /* Text of the last error in this thread ("" if none). */
@@ -125,6 +137,18 @@ sfmg_status sfmg_diag(sfmg_level lv, int32_t bc, double* d_diag, int64_t n, void
  * splitmix64(seed) start vector, boundary zeroed (R9).  Syncs. */
 sfmg_status sfmg_lambda_max(sfmg_level lv, int32_t iters, uint64_t seed, double* h_lambda,
                             void* stream);
+/* lambda_max of D^{-1} A_D by `steps` Arnoldi iterations in the D-inner product <x,y>_D =
+ * sum d x y (D^{-1} A_D is self-adjoint in it, so H is symmetric tridiagonal up to rounding;
+ * Gram-Schmidt repeated once per step), from the same splitmix64(seed) start vector as
+ * sfmg_lambda_max; the estimate is the largest eigenvalue of the k x k matrix H (k = steps, or
+ * fewer if the Krylov space is exhausted) (R26).  d_work: caller-owned
+ * device scratch of (steps + 2) * N doubles.  Syncs. */
+sfmg_status sfmg_lambda_arnoldi(sfmg_level lv, int32_t steps, uint64_t seed, double* d_work,
+                                double* h_lambda, void* stream);
+/* `steps` damped point-Jacobi steps x += omega D^{-1} (b - A_D x), one
+ * operator apply each; d_x in/out. */
+sfmg_status sfmg_jacobi(sfmg_level lv, const double* d_b, double* d_x, int64_t n, int32_t steps,
+                        double omega, void* stream);
 /* One degree-`degree` Chebyshev-accelerated Jacobi application to A_D x = b on the interval
  * [lam_lo, lam_hi] of D^{-1} A_D (R7, R10): `degree` steps, each one
  * operator apply.  d_x is the initial guess on input and the smoothed iterate on output. */
@@ -149,8 +173,10 @@ sfmg_status sfmg_cheb_host(sfmg_level lv, const double* h_b, double* h_x, int64_
 sfmg_status sfmg_profile_enable(sfmg_level lv, int32_t enable);
 sfmg_status sfmg_profile_read(sfmg_level lv, double* ms, int64_t* launches, int32_t reset);
 
-/* ---------------------------------------------------------------- p-transfer */
-/* fine.order == 2 coarse.order on the same element grid, else SFMG_E_PCOARSEN.
+/* ---------------------------------------------------------------- transfer */
+/* p pair: fine.order == 2 coarse.order on the same element grid (coarse.order <= 8); or h pair:
+ * both order 1, fine.ne == 2 coarse.ne in every direction (nesting in reference-
+ * lattice coordinates, R25).  Anything else: SFMG_E_PCOARSEN.
  * prolong: d_uf = P0 d_uc with P0 = M_f P M_c, P_gJ = phi^{coarse}_J(xi(g)) (eq. (7)).
  * restrict: d_rc = P0^T d_rf (R12).  Vectors sized N_coarse / N_fine. */
 sfmg_status sfmg_prolong(sfmg_level coarse, sfmg_level fine, const double* d_uc, double* d_uf,
@@ -160,8 +186,10 @@ sfmg_status sfmg_restrict(sfmg_level coarse, sfmg_level fine, const double* d_rf
 
 /* ---------------------------------------------------------------- hierarchy */
 sfmg_status sfmg_hier_query(const sfmg_problem* fine, const sfmg_mg_params* mg, size_t* ws_bytes);
-/* Build levels p, p/2, ..., 1 (geometry rediscretised per level, R20), their diagonals and
- * lambda_max estimates.  Syncs. */
+/* Build levels p, p/2, ..., 1 (geometry rediscretised per level, R20), then mg->h_levels p = 1
+ * levels on meshes ne/2, ne/4, ..., their diagonals and lambda_max estimates (power iteration or
+ * Arnoldi per mg->lambda_method).  Syncs.  SFMG_E_PCOARSEN if p is not a power of two or a mesh
+ * size is not divisible by 2^h_levels. */
 sfmg_status sfmg_hier_create(const sfmg_problem* fine, const sfmg_mg_params* mg, void* d_ws,
                              size_t ws_bytes, void* stream, sfmg_hier* out);
 sfmg_status sfmg_hier_destroy(sfmg_hier h);
@@ -169,8 +197,8 @@ sfmg_status sfmg_hier_info(sfmg_hier h, int32_t* n_levels, int64_t* n_dofs_fine)
 /* Level l (0 = finest) as a level handle owned by the hierarchy (do not destroy). */
 sfmg_status sfmg_hier_level(sfmg_hier h, int32_t l, sfmg_level* out);
 sfmg_status sfmg_hier_lambda(sfmg_hier h, int32_t l, double* h_lambda);
-/* x = V(b) from x = 0: per level nu_pre Chebyshev applications, residual, restriction,
- * recursion, prolongation + correction, nu_post applications; coarsest (p = 1) by CG
+/* x = V(b) from x = 0: per level nu_pre smoothing applications (Chebyshev or Jacobi), residual,
+ * restriction, recursion, prolongation + correction, nu_post applications; coarsest by CG
  * (R11, R13).  No host synchronisation. */
 sfmg_status sfmg_vcycle(sfmg_hier h, const double* d_b, double* d_x, void* stream);
 /* mode 0: MG as solver, x <- x + V(b - A x); mode 1: MG-preconditioned CG (Algorithm 1,

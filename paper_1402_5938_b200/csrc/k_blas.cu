@@ -161,6 +161,30 @@ __global__ void k_axpy1(double* x, const double* __restrict__ y, long long n) {
     x[i] += y[i];
 }
 
+// Arnoldi in the D-inner product (R26): scalars[slot] = sum a b / dinv = <a, b>_D
+__global__ void __launch_bounds__(kRedThreads) k_dotw(RedScratch r, const double* __restrict__ a,
+                                                      const double* __restrict__ b,
+                                                      const double* __restrict__ dinv, long long n, int slot) {
+  double v[1] = {0.0};
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    v[0] += a[i] * b[i] / dinv[i];
+  double f[1];
+  if (grid_reduce<1>(v, r, f)) r.scalars[slot] = f[0];
+}
+// y -= scalars[slot] x  (Gram-Schmidt step with the coefficient left on the device)
+__global__ void k_sub_scaled_dev(const double* __restrict__ scal, int slot, const double* __restrict__ x, double* y,
+                                 long long n) {
+  const double a = scal[slot];
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    y[i] -= a * x[i];
+}
+// y = a x (a * dinv) elementwise: w = D^{-1} (A q) when d = dinv, a = 1
+__global__ void k_scale_mul(double a, const double* __restrict__ x, const double* __restrict__ d, double* y,
+                            long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    y[i] = a * x[i] * (d ? d[i] : 1.0);
+}
+
 static int vgrid(long long n) {
   long long b = (n + 255) / 256;
   if (b > 148LL * 16) b = 148LL * 16;
@@ -205,6 +229,20 @@ cudaError_t launch_copy(const double* a, double* b, long long n, cudaStream_t s)
 }
 cudaError_t launch_residual(const double* b, const double* y, double* r, long long n, cudaStream_t s) {
   k_residual<<<vgrid(n), 256, 0, s>>>(b, y, r, n);
+  return cudaGetLastError();
+}
+cudaError_t launch_dotw(const RedScratch& r, const double* a, const double* b, const double* dinv, long long n,
+                        int slot, cudaStream_t s) {
+  k_dotw<<<kRedBlocks, kRedThreads, 0, s>>>(r, a, b, dinv, n, slot);
+  return cudaGetLastError();
+}
+cudaError_t launch_sub_scaled_dev(const RedScratch& r, int slot, const double* x, double* y, long long n,
+                                  cudaStream_t s) {
+  k_sub_scaled_dev<<<vgrid(n), 256, 0, s>>>(r.scalars, slot, x, y, n);
+  return cudaGetLastError();
+}
+cudaError_t launch_scale_mul(double a, const double* x, const double* d, double* y, long long n, cudaStream_t s) {
+  k_scale_mul<<<vgrid(n), 256, 0, s>>>(a, x, d, y, n);
   return cudaGetLastError();
 }
 cudaError_t launch_axpy1(double* x, const double* y, long long n, cudaStream_t s) {

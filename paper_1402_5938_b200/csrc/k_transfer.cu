@@ -1,4 +1,5 @@
-// p-multigrid transfer kernels for sm_100a (eq. (7)).
+// Multigrid transfer kernels for sm_100a (eq. (7)): p-transfer
+// p/2 <-> p on one element grid, and (NEXT-1) h-transfer at p = 1 between nested element grids.
 //
 // Prolongation p/2 -> p on one element grid: P_gJ = phi^{p/2}_J(xi(g)); per element this is the
 // tensor contraction u_f(i,j,k) = sum_{abc} I[i][a] I[j][b] I[k][c] u_c(a,b,c) with the 1-D
@@ -207,6 +208,93 @@ cudaError_t launch_restrict(const MeshDev& mc, const MeshDev& mf, const double* 
     case 8: return restrict_p<8>(mc, mf, rf, rc, s);
   }
   return cudaErrorInvalidValue;
+}
+
+// ------------------------------------------------------------------------------------------
+// h-transfer at p = 1 between nested element grids (fine ne = 2 coarse ne; eq. (7) across
+// meshes; nesting in reference-lattice coordinates, R25).  On the p = 1 lattices the
+// coarse trilinear basis evaluated at the fine nodes gives, per axis, weight 1 for fine index
+// I = 2 Ic and 1/2 for I = 2 Ic +- 1.  Both directions are gathers (thread per output node): no
+// atomics, deterministic.  P0 = M_f P M_c (R12).
+
+struct HW {   // the (<= 2) coarse indices and weights of one fine lattice index
+  int i0, i1;
+  double w0, w1;
+};
+__device__ __forceinline__ HW hweights(int I) {
+  HW h;
+  if ((I & 1) == 0) { h.i0 = h.i1 = I >> 1; h.w0 = 1.0; h.w1 = 0.0; }
+  else { h.i0 = (I - 1) >> 1; h.i1 = (I + 1) >> 1; h.w0 = h.w1 = 0.5; }
+  return h;
+}
+
+__global__ void k_prolong_h(MeshDev mc, MeshDev mf, const double* __restrict__ uc, double* __restrict__ uf,
+                            int add) {
+  const long long n = mf.N;
+  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < n; g += (long long)gridDim.x * blockDim.x) {
+    const int I = (int)(g % mf.Mx), J = (int)((g / mf.Mx) % mf.My), K = (int)(g / ((long long)mf.Mx * mf.My));
+    if (I == 0 || I == mf.Mx - 1 || J == 0 || J == mf.My - 1 || K == 0 || K == mf.Mz - 1) {
+      if (!add) uf[g] = 0.0;
+      continue;
+    }
+    const HW hx = hweights(I), hy = hweights(J), hz = hweights(K);
+    const int ix[2] = {hx.i0, hx.i1}, iy[2] = {hy.i0, hy.i1}, iz[2] = {hz.i0, hz.i1};
+    const double wx[2] = {hx.w0, hx.w1}, wy[2] = {hy.w0, hy.w1}, wz[2] = {hz.w0, hz.w1};
+    double s = 0.0;
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+      for (int b = 0; b < 2; ++b)
+#pragma unroll
+        for (int a = 0; a < 2; ++a) {
+          const double w = wx[a] * wy[b] * wz[c];
+          const int Ic = ix[a], Jc = iy[b], Kc = iz[c];
+          if (w == 0.0 || Ic == 0 || Ic == mc.Mx - 1 || Jc == 0 || Jc == mc.My - 1 || Kc == 0 || Kc == mc.Mz - 1)
+            continue;   // M_c: coarse boundary values read as zero
+          s += w * uc[Ic + (long long)mc.Mx * (Jc + (long long)mc.My * Kc)];
+        }
+    if (add) uf[g] += s; else uf[g] = s;
+  }
+}
+
+__global__ void k_restrict_h(MeshDev mc, MeshDev mf, const double* __restrict__ rf, double* __restrict__ rc) {
+  const long long n = mc.N;
+  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < n; g += (long long)gridDim.x * blockDim.x) {
+    const int I = (int)(g % mc.Mx), J = (int)((g / mc.Mx) % mc.My), K = (int)(g / ((long long)mc.Mx * mc.My));
+    if (I == 0 || I == mc.Mx - 1 || J == 0 || J == mc.My - 1 || K == 0 || K == mc.Mz - 1) {
+      rc[g] = 0.0;
+      continue;
+    }
+    double s = 0.0;
+    for (int dz = -1; dz <= 1; ++dz)
+      for (int dy = -1; dy <= 1; ++dy)
+        for (int dx = -1; dx <= 1; ++dx) {
+          const int If = 2 * I + dx, Jf = 2 * J + dy, Kf = 2 * K + dz;
+          if (If == 0 || If == mf.Mx - 1 || Jf == 0 || Jf == mf.My - 1 || Kf == 0 || Kf == mf.Mz - 1) continue;
+          const double w = (dx ? 0.5 : 1.0) * (dy ? 0.5 : 1.0) * (dz ? 0.5 : 1.0);   // M_f r_f
+          s += w * rf[If + (long long)mf.Mx * (Jf + (long long)mf.My * Kf)];
+        }
+    rc[g] = s;
+  }
+}
+
+static unsigned hgrid(long long n) {
+  long long b = (n + 255) / 256;
+  if (b > 148LL * 16) b = 148LL * 16;
+  return (unsigned)(b < 1 ? 1 : b);
+}
+
+cudaError_t launch_prolong_h(const MeshDev& mc, const MeshDev& mf, const double* uc, double* uf, int add,
+                             cudaStream_t s) {
+  if (mc.p != 1 || mf.p != 1) return cudaErrorInvalidValue;
+  k_prolong_h<<<hgrid(mf.N), 256, 0, s>>>(mc, mf, uc, uf, add);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_restrict_h(const MeshDev& mc, const MeshDev& mf, const double* rf, double* rc, cudaStream_t s) {
+  if (mc.p != 1 || mf.p != 1) return cudaErrorInvalidValue;
+  k_restrict_h<<<hgrid(mc.N), 256, 0, s>>>(mc, mf, rf, rc);
+  return cudaGetLastError();
 }
 
 }  // namespace sfmg

@@ -2,6 +2,7 @@
 // orchestration of the kernels (Chebyshev recurrence scalars, V-cycle recursion, Algorithm 1).
 // Host code only launches kernels on the caller's stream; no arithmetic of the method runs here
 // except the scalar Chebyshev recurrence coefficients (R7).
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -192,6 +193,93 @@ static cudaError_t op_cheb(sfmg_level_s* lv, const double* b, double* x, int K, 
   return cudaSuccess;
 }
 
+// `steps` damped point-Jacobi steps x += omega D^{-1} (b - A_D x): the
+// Chebyshev update kernel with c1 = 0, c2 = omega (it also re-initialises y for the next apply).
+static cudaError_t op_jacobi(sfmg_level_s* lv, const double* b, double* x, int steps, double omega,
+                             cudaStream_t s) {
+  for (int k = 0; k < steps; ++k) {
+    cudaError_t e = (k == 0) ? op_apply(lv, 0, x, lv->y, s) : element_kernel(lv, 0, x, lv->y, 2, 0, s);
+    if (e) return e;
+    if ((e = launch_cheb_update(lv->m, x, x, x, b, lv->y, lv->dinv, 0.0, omega, s))) return e;
+  }
+  return cudaSuccess;
+}
+
+// Largest eigenvalue of the symmetric tridiagonal matrix (a[0..k), off-diagonal b[0..k-1)) by
+// Sturm-sequence bisection (count of negative pivots of T - x I = number of eigenvalues < x).
+static double tridiag_max_eig(const std::vector<double>& a, const std::vector<double>& b) {
+  const int k = (int)a.size();
+  double lo = 1e300, hi = -1e300;
+  for (int i = 0; i < k; ++i) {   // Gershgorin interval
+    const double r = (i > 0 ? std::fabs(b[i - 1]) : 0.0) + (i + 1 < k ? std::fabs(b[i]) : 0.0);
+    lo = std::min(lo, a[i] - r);
+    hi = std::max(hi, a[i] + r);
+  }
+  auto below = [&](double x) {
+    int c = 0;
+    double q = 1.0;
+    for (int i = 0; i < k; ++i) {
+      q = (a[i] - x) - (i > 0 ? b[i - 1] * b[i - 1] / q : 0.0);
+      if (q == 0.0) q = -1e-300;
+      if (q < 0.0) ++c;
+    }
+    return c;
+  };
+  for (int it = 0; it < 300 && hi - lo > 4e-16 * std::max(std::fabs(lo), std::fabs(hi)); ++it) {
+    const double mid = 0.5 * (lo + hi);
+    if (below(mid) == k) hi = mid; else lo = mid;
+  }
+  return 0.5 * (lo + hi);
+}
+
+// lambda_max(D^{-1} A_D) from m Arnoldi steps in the D-inner product (R26):
+// modified Gram-Schmidt repeated once per step, coefficients kept on the device between kernels
+// (slots 14.. of the level's scalars) and read back once per pass to accumulate H.  work: (m + 2) N.
+static sfmg_status arnoldi_lambda(sfmg_level_s* lv, int m, uint64_t seed, double* work, double* lam,
+                                  cudaStream_t s) {
+  const long long N = lv->N;
+  double* Q = work;                   // q_0 .. q_m
+  double* w = work + (size_t)(m + 1) * N;
+  double* sc = lv->red.scalars;
+  double host[32];
+  CK(launch_power_start(lv->m, seed, Q, lv->y, s));           // q_0: seeded, boundary zero (R9)
+  CK(launch_dotw(lv->red, Q, Q, lv->dinv, N, 14, s));
+  CK(cudaMemcpyAsync(host, sc + 14, sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (!(host[0] > 0.0)) { set_error("Arnoldi start vector is zero (no interior dofs)"); return SFMG_E_ARG; }
+  CK(launch_scale_mul(1.0 / std::sqrt(host[0]), Q, nullptr, Q, N, s));
+  std::vector<double> H((size_t)(m + 1) * m, 0.0);
+  int k = 0;
+  for (int j = 0; j < m; ++j) {
+    double* qj = Q + (size_t)j * N;
+    CK(op_apply(lv, 0, qj, lv->y, s));
+    CK(launch_scale_mul(1.0, lv->y, lv->dinv, w, N, s));      // w = D^{-1} A_D q_j
+    CK(launch_dotw(lv->red, w, w, lv->dinv, N, 13, s));
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int i = 0; i <= j; ++i) {
+        CK(launch_dotw(lv->red, w, Q + (size_t)i * N, lv->dinv, N, 14 + i, s));
+        CK(launch_sub_scaled_dev(lv->red, 14 + i, Q + (size_t)i * N, w, N, s));
+      }
+      CK(cudaMemcpyAsync(host, sc + 14, sizeof(double) * (j + 1), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      for (int i = 0; i <= j; ++i) H[(size_t)i * m + j] += host[i];
+    }
+    CK(launch_dotw(lv->red, w, w, lv->dinv, N, 12, s));
+    CK(cudaMemcpyAsync(host, sc + 12, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const double hn = std::sqrt(host[0]), wn0 = std::sqrt(host[1]);
+    k = j + 1;
+    H[(size_t)(j + 1) * m + j] = hn;
+    if (hn <= 1e-10 * wn0) break;   // Krylov space exhausted
+    CK(launch_scale_mul(1.0 / hn, w, nullptr, Q + (size_t)(j + 1) * N, N, s));
+  }
+  std::vector<double> a(k), b(k > 0 ? k - 1 : 0);
+  for (int i = 0; i < k; ++i) a[i] = H[(size_t)i * m + i];
+  for (int i = 0; i + 1 < k; ++i) b[i] = 0.5 * (H[(size_t)i * m + i + 1] + H[(size_t)(i + 1) * m + i]);
+  *lam = tridiag_max_eig(a, b);
+  return SFMG_OK;
+}
+
 }  // namespace sfmg
 
 using namespace sfmg;
@@ -322,6 +410,26 @@ sfmg_status sfmg_cheb(sfmg_level lv, const double* d_b, double* d_x, int64_t n, 
   return SFMG_OK;
 }
 
+sfmg_status sfmg_lambda_arnoldi(sfmg_level lv, int32_t steps, uint64_t seed, double* d_work, double* h_lambda,
+                                void* stream) {
+  if (!lv || !h_lambda || !d_work || steps < 1 || steps > 16) {
+    set_error("bad argument to sfmg_lambda_arnoldi (steps 1..16, work of (steps + 2) N doubles)");
+    return SFMG_E_ARG;
+  }
+  return arnoldi_lambda(lv, steps, seed, d_work, h_lambda, (cudaStream_t)stream);
+}
+
+sfmg_status sfmg_jacobi(sfmg_level lv, const double* d_b, double* d_x, int64_t n, int32_t steps, double omega,
+                        void* stream) {
+  if (!lv || !d_b || !d_x || d_b == d_x || steps < 0 || !(omega > 0.0 && omega < 2.0)) {
+    set_error("bad argument to sfmg_jacobi");
+    return SFMG_E_ARG;
+  }
+  if (n != lv->N) { set_error("vector length != N"); return SFMG_E_ARG; }
+  CK(op_jacobi(lv, d_b, d_x, steps, omega, (cudaStream_t)stream));
+  return SFMG_OK;
+}
+
 sfmg_status sfmg_load_vector(sfmg_level lv, int32_t rhs_id, double* d_f, int64_t n, void* stream) {
   if (!lv || !d_f || rhs_id != 1) return SFMG_E_ARG;
   if (n != lv->N) return SFMG_E_ARG;
@@ -355,48 +463,83 @@ sfmg_status sfmg_cheb_host(sfmg_level lv, const double* h_b, double* h_x, int64_
   return SFMG_OK;
 }
 
-static sfmg_status check_pair(sfmg_level c, sfmg_level f) {
+// 1: p pair (fine.p = 2 coarse.p <= 16, same element grid); 2: h pair (p = 1 both, fine ne = 2 coarse ne)
+static int pair_kind(const MeshDev& c, const MeshDev& f) {
+  if (f.p == 2 * c.p && c.p <= 8 && f.nex == c.nex && f.ney == c.ney && f.nez == c.nez) return 1;
+  if (c.p == 1 && f.p == 1 && f.nex == 2 * c.nex && f.ney == 2 * c.ney && f.nez == 2 * c.nez) return 2;
+  return 0;
+}
+
+static sfmg_status check_pair(sfmg_level c, sfmg_level f, int* kind) {
   if (!c || !f) return SFMG_E_ARG;
-  if (f->p != 2 * c->p || f->m.nex != c->m.nex || f->m.ney != c->m.ney || f->m.nez != c->m.nez || c->p > 8) {
-    set_error("levels are not (p/2, p) on one element grid");
+  *kind = pair_kind(c->m, f->m);
+  if (!*kind) {
+    set_error("levels are neither (p/2, p) on one element grid nor (ne/2, ne) at p = 1");
     return SFMG_E_PCOARSEN;
   }
   return SFMG_OK;
 }
 
+static cudaError_t transfer_prolong(const MeshDev& c, const MeshDev& f, const double* uc, double* uf, int add,
+                                    cudaStream_t s) {
+  return pair_kind(c, f) == 2 ? launch_prolong_h(c, f, uc, uf, add, s) : launch_prolong(c, f, uc, uf, add, s);
+}
+static cudaError_t transfer_restrict(const MeshDev& c, const MeshDev& f, const double* rf, double* rc,
+                                     cudaStream_t s) {
+  return pair_kind(c, f) == 2 ? launch_restrict_h(c, f, rf, rc, s) : launch_restrict(c, f, rf, rc, s);
+}
+
 sfmg_status sfmg_prolong(sfmg_level coarse, sfmg_level fine, const double* d_uc, double* d_uf, void* stream) {
-  sfmg_status st = check_pair(coarse, fine);
+  int kind = 0;
+  sfmg_status st = check_pair(coarse, fine, &kind);
   if (st) return st;
   if (!d_uc || !d_uf) return SFMG_E_ARG;
-  CK(upload_interp_tables(coarse->p, (cudaStream_t)stream));
-  CK(launch_prolong(coarse->m, fine->m, d_uc, d_uf, 0, (cudaStream_t)stream));
+  if (kind == 1) CK(upload_interp_tables(coarse->p, (cudaStream_t)stream));
+  CK(transfer_prolong(coarse->m, fine->m, d_uc, d_uf, 0, (cudaStream_t)stream));
   return SFMG_OK;
 }
 
 sfmg_status sfmg_restrict(sfmg_level coarse, sfmg_level fine, const double* d_rf, double* d_rc, void* stream) {
-  sfmg_status st = check_pair(coarse, fine);
+  int kind = 0;
+  sfmg_status st = check_pair(coarse, fine, &kind);
   if (st) return st;
   if (!d_rf || !d_rc) return SFMG_E_ARG;
-  CK(upload_interp_tables(coarse->p, (cudaStream_t)stream));
-  CK(launch_restrict(coarse->m, fine->m, d_rf, d_rc, (cudaStream_t)stream));
+  if (kind == 1) CK(upload_interp_tables(coarse->p, (cudaStream_t)stream));
+  CK(transfer_restrict(coarse->m, fine->m, d_rf, d_rc, (cudaStream_t)stream));
   return SFMG_OK;
 }
 
 // ------------------------------------------------------------------------------ hierarchy
 
-static sfmg_status hier_orders(const sfmg_problem* fine, std::vector<int>& orders) {
-  orders.clear();
+// Level problems of the hierarchy: orders p, p/2, ..., 1 on the fine mesh, then
+// mg->h_levels p = 1 levels on meshes ne/2, ne/4, ....
+static sfmg_status hier_specs(const sfmg_problem* fine, const sfmg_mg_params* mg, std::vector<sfmg_problem>& out) {
+  out.clear();
   for (int q = fine->order;; q /= 2) {
-    orders.push_back(q);
+    sfmg_problem pr = *fine;
+    pr.order = q;
+    out.push_back(pr);
     if (q == 1) break;
     if (q % 2) { set_error("order cannot be p-coarsened to 1 by halving"); return SFMG_E_PCOARSEN; }
+  }
+  for (int j = 1; j <= mg->h_levels; ++j) {
+    sfmg_problem pr = out.back();
+    if (pr.nex % 2 || pr.ney % 2 || pr.nez % 2) {
+      set_error("mesh cannot be h-coarsened h_levels times (element counts must be divisible by 2^h_levels)");
+      return SFMG_E_PCOARSEN;
+    }
+    pr.nex /= 2; pr.ney /= 2; pr.nez /= 2;
+    out.push_back(pr);
   }
   return SFMG_OK;
 }
 
 static sfmg_status check_mg(const sfmg_mg_params* mg) {
   if (!mg || mg->nu_pre < 0 || mg->nu_post < 0 || mg->cheb_degree < 1 || !(mg->eig_hi_frac > mg->eig_lo_frac) ||
-      !(mg->eig_lo_frac > 0) || mg->power_iters < 1 || !(mg->coarse_rtol > 0) || mg->coarse_max_iter < 1) {
+      !(mg->eig_lo_frac > 0) || mg->power_iters < 1 || !(mg->coarse_rtol > 0) || mg->coarse_max_iter < 1 ||
+      (mg->smoother != 0 && mg->smoother != 1) || (mg->smoother == 1 && !(mg->jacobi_omega > 0 && mg->jacobi_omega < 2)) ||
+      (mg->lambda_method != 0 && mg->lambda_method != 1) || (mg->lambda_method == 1 && mg->power_iters > 16) ||
+      mg->h_levels < 0 || mg->h_levels > 20) {
     set_error("bad multigrid parameters");
     return SFMG_E_ARG;
   }
@@ -407,15 +550,14 @@ sfmg_status sfmg_hier_query(const sfmg_problem* fine, const sfmg_mg_params* mg, 
   sfmg_status st = check_problem(fine);
   if (st) return st;
   if ((st = check_mg(mg))) return st;
-  std::vector<int> orders;
-  if ((st = hier_orders(fine, orders))) return st;
+  std::vector<sfmg_problem> specs;
+  if ((st = hier_specs(fine, mg, specs))) return st;
   size_t total = 0;
-  for (size_t l = 0; l < orders.size(); ++l) {
-    sfmg_problem q = *fine;
-    q.order = orders[l];
-    MeshDev m = make_mesh(&q);
+  for (size_t l = 0; l < specs.size(); ++l) {
+    MeshDev m = make_mesh(&specs[l]);
     total += level_layout(m).total + 3 * align_up(sizeof(double) * m.N);
     if (l == 0) total += 4 * align_up(sizeof(double) * m.N);
+    if (l == 0 && mg->lambda_method == 1) total += align_up(sizeof(double) * (size_t)(mg->power_iters + 2) * m.N);
   }
   if (ws_bytes) *ws_bytes = total;
   return SFMG_OK;
@@ -441,15 +583,15 @@ sfmg_status sfmg_hier_create(const sfmg_problem* fine, const sfmg_mg_params* mg,
   if (!out) return SFMG_E_ARG;
   if (!d_ws || ((uintptr_t)d_ws & 255) || ws_bytes < need) { set_error("workspace too small"); return SFMG_E_WORKSPACE; }
   cudaStream_t s = (cudaStream_t)stream;
-  std::vector<int> orders;
-  hier_orders(fine, orders);
+  std::vector<sfmg_problem> specs;
+  hier_specs(fine, mg, specs);
   sfmg_hier_s* h = new sfmg_hier_s();
   h->mg = *mg;
   h->fine_applies = 0;
   char* base = (char*)d_ws;
-  for (size_t l = 0; l < orders.size(); ++l) {
-    sfmg_problem q = *fine;
-    q.order = orders[l];
+  double* arn_work = nullptr;
+  for (size_t l = 0; l < specs.size(); ++l) {
+    const sfmg_problem& q = specs[l];
     MeshDev m = make_mesh(&q);
     LevelLayout L = level_layout(m);
     sfmg_level_s* lv = nullptr;
@@ -467,16 +609,21 @@ sfmg_status sfmg_hier_create(const sfmg_problem* fine, const sfmg_mg_params* mg,
       h->pz = (double*)base; base += vb;
       h->pp = (double*)base; base += vb;
       h->ph = (double*)base; base += vb;
+      if (mg->lambda_method == 1) {
+        arn_work = (double*)base;
+        base += align_up(sizeof(double) * (size_t)(mg->power_iters + 2) * m.N);
+      }
     }
-    if (orders[l] > 1) {
-      cudaError_t e = upload_interp_tables(orders[l] / 2, s);
+    if (l + 1 < specs.size() && specs[l + 1].order * 2 == q.order) {
+      cudaError_t e = upload_interp_tables(q.order / 2, s);
       if (e) { sfmg_hier_destroy(h); return cuda_fail(e, "interp tables"); }
     }
   }
   h->lam.assign(h->lv.size(), 0.0);
   for (size_t l = 0; l + 1 < h->lv.size(); ++l) {
     double lam = 0.0;
-    st = sfmg_lambda_max(h->lv[l], mg->power_iters, mg->power_seed, &lam, stream);
+    st = (mg->lambda_method == 1) ? arnoldi_lambda(h->lv[l], mg->power_iters, mg->power_seed, arn_work, &lam, s)
+                                  : sfmg_lambda_max(h->lv[l], mg->power_iters, mg->power_seed, &lam, stream);
     if (st) { sfmg_hier_destroy(h); return st; }
     h->lam[l] = lam;
   }
@@ -516,22 +663,27 @@ static cudaError_t vcycle_level(sfmg_hier_s* h, size_t l, const double* b, doubl
                             mg.coarse_max_iter, s);
   }
   const double lo = mg.eig_lo_frac * h->lam[l], hi = mg.eig_hi_frac * h->lam[l];
-  if ((e = cudaMemsetAsync(x, 0, sizeof(double) * lv->N, s))) return e;
-  for (int i = 0; i < mg.nu_pre; ++i) {
-    if ((e = op_cheb(lv, b, x, mg.cheb_degree, lo, hi, s))) return e;
+  // one smoothing application: a degree-K Chebyshev polynomial or one damped Jacobi step
+  auto smooth = [&]() -> cudaError_t {
+    if (mg.smoother == 1) {
+      if (l == 0) h->fine_applies += 1;
+      return op_jacobi(lv, b, x, 1, mg.jacobi_omega, s);
+    }
     if (l == 0) h->fine_applies += mg.cheb_degree;
-  }
+    return op_cheb(lv, b, x, mg.cheb_degree, lo, hi, s);
+  };
+  if ((e = cudaMemsetAsync(x, 0, sizeof(double) * lv->N, s))) return e;
+  for (int i = 0; i < mg.nu_pre; ++i)
+    if ((e = smooth())) return e;
   if ((e = op_apply(lv, 0, x, lv->y, s))) return e;
   if (l == 0) h->fine_applies += 1;
   if ((e = launch_residual(b, lv->y, h->r[l], lv->N, s))) return e;
   sfmg_level_s* c = h->lv[l + 1];
-  if ((e = launch_restrict(c->m, lv->m, h->r[l], h->b[l + 1], s))) return e;
+  if ((e = transfer_restrict(c->m, lv->m, h->r[l], h->b[l + 1], s))) return e;
   if ((e = vcycle_level(h, l + 1, h->b[l + 1], h->x[l + 1], s))) return e;
-  if ((e = launch_prolong(c->m, lv->m, h->x[l + 1], x, 1, s))) return e;
-  for (int i = 0; i < mg.nu_post; ++i) {
-    if ((e = op_cheb(lv, b, x, mg.cheb_degree, lo, hi, s))) return e;
-    if (l == 0) h->fine_applies += mg.cheb_degree;
-  }
+  if ((e = transfer_prolong(c->m, lv->m, h->x[l + 1], x, 1, s))) return e;
+  for (int i = 0; i < mg.nu_post; ++i)
+    if ((e = smooth())) return e;
   return cudaSuccess;
 }
 

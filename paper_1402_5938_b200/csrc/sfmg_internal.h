@@ -126,6 +126,14 @@ cudaError_t launch_pcg_p(const RedScratch& red, double* p, const double* z, int 
                          cudaStream_t s);
 // x += y
 cudaError_t launch_axpy1(double* x, const double* y, long long n, cudaStream_t s);
+// scalars[slot] = sum a b / dinv  (<a, b>_D, Arnoldi R26)
+cudaError_t launch_dotw(const RedScratch& r, const double* a, const double* b, const double* dinv, long long n,
+                        int slot, cudaStream_t s);
+// y -= scalars[slot] x
+cudaError_t launch_sub_scaled_dev(const RedScratch& r, int slot, const double* x, double* y, long long n,
+                                  cudaStream_t s);
+// y = a x (* d elementwise if d != null)
+cudaError_t launch_scale_mul(double a, const double* x, const double* d, double* y, long long n, cudaStream_t s);
 
 // ---- transfer (k_transfer.cu)
 cudaError_t upload_interp_tables(int pc, cudaStream_t s);
@@ -134,6 +142,10 @@ cudaError_t launch_prolong(const MeshDev& mc, const MeshDev& mf, const double* u
                            cudaStream_t s);
 // rc = P0^T rf (rc zeroed inside)
 cudaError_t launch_restrict(const MeshDev& mc, const MeshDev& mf, const double* rf, double* rc, cudaStream_t s);
+// h pair at p = 1 (fine ne = 2 coarse ne): uf = P0 uc (add: uf += P0 uc); rc = P0^T rf (gathers, no atomics)
+cudaError_t launch_prolong_h(const MeshDev& mc, const MeshDev& mf, const double* uc, double* uf, int add,
+                             cudaStream_t s);
+cudaError_t launch_restrict_h(const MeshDev& mc, const MeshDev& mf, const double* rf, double* rc, cudaStream_t s);
 
 void set_error(const std::string& s);
 

@@ -43,7 +43,9 @@ class _Problem(C.Structure):
 class _MgParams(C.Structure):
     _fields_ = [("nu_pre", C.c_int32), ("nu_post", C.c_int32), ("cheb_degree", C.c_int32),
                 ("eig_lo_frac", C.c_double), ("eig_hi_frac", C.c_double), ("power_iters", C.c_int32),
-                ("power_seed", C.c_uint64), ("coarse_rtol", C.c_double), ("coarse_max_iter", C.c_int32)]
+                ("power_seed", C.c_uint64), ("coarse_rtol", C.c_double), ("coarse_max_iter", C.c_int32),
+                ("smoother", C.c_int32), ("jacobi_omega", C.c_double), ("lambda_method", C.c_int32),
+                ("h_levels", C.c_int32)]
 
 
 class _Report(C.Structure):
@@ -69,6 +71,8 @@ _SIG = {
     "sfmg_diag": ([_vp, _i32, _vp, _i64, _vp], C.c_int),
     "sfmg_lambda_max": ([_vp, _i32, _u64, _P(_d), _vp], C.c_int),
     "sfmg_cheb": ([_vp, _vp, _vp, _i64, _i32, _d, _d, _vp], C.c_int),
+    "sfmg_lambda_arnoldi": ([_vp, _i32, _u64, _vp, _P(_d), _vp], C.c_int),
+    "sfmg_jacobi": ([_vp, _vp, _vp, _i64, _i32, _d, _vp], C.c_int),
     "sfmg_load_vector": ([_vp, _i32, _vp, _i64, _vp], C.c_int),
     "sfmg_apply_host": ([_vp, _i32, _vp, _vp, _i64, _vp], C.c_int),
     "sfmg_cheb_host": ([_vp, _vp, _vp, _i64, _i32, _d, _d, _vp], C.c_int),
@@ -207,6 +211,20 @@ class Level:
         _ck(_lib.sfmg_lambda_max(self.h, iters, seed, C.byref(lam), _stream(stream)), "sfmg_lambda_max")
         return lam.value
 
+    def lambda_arnoldi(self, steps=10, seed=12345, stream=None):
+        """lambda_max(D^-1 A_D) by `steps` Arnoldi iterations in the D-inner product (R26)."""
+        work = torch.empty((steps + 2) * self.N, dtype=torch.float64, device=self.device)
+        lam = _d()
+        _ck(_lib.sfmg_lambda_arnoldi(self.h, steps, seed, C.c_void_p(work.data_ptr()), C.byref(lam),
+                                     _stream(stream)), "sfmg_lambda_arnoldi")
+        return lam.value
+
+    def jacobi(self, b, x, steps, omega=2.0 / 3.0, stream=None):
+        """In place on x: `steps` damped point-Jacobi steps."""
+        _ck(_lib.sfmg_jacobi(self.h, _dptr(b, self.N), _dptr(x, self.N), self.N, steps, omega, _stream(stream)),
+            "sfmg_jacobi")
+        return x
+
     def cheb(self, b, x, degree, lam_lo, lam_hi, stream=None):
         """In place on x (initial guess in, smoothed iterate out)."""
         _ck(_lib.sfmg_cheb(self.h, _dptr(b, self.N), _dptr(x, self.N), self.N, degree, lam_lo, lam_hi,
@@ -278,7 +296,9 @@ def restrict(coarse: Level, fine: Level, rf, rc=None, stream=None):
 
 @dataclass
 class MgParams:
-    """p-MG parameters (BASELINE config 5 defaults; R7-R11, R13)."""
+    """p-MG parameters (BASELINE config 5 defaults; R7-R11, R13).  smoother 1 = damped Jacobi
+    (jacobi_omega), lambda_method 1 = Arnoldi, h_levels = geometric coarsenings after p = 1: the
+    paper's own settings (see MgParams.paper())."""
     nu_pre: int = 2
     nu_post: int = 2
     cheb_degree: int = 4
@@ -288,10 +308,26 @@ class MgParams:
     power_seed: int = 12345
     coarse_rtol: float = 1e-10
     coarse_max_iter: int = 10000
+    smoother: int = 0
+    jacobi_omega: float = 2.0 / 3.0
+    lambda_method: int = 0
+    h_levels: int = 0
+
+    @staticmethod
+    def paper(smoother="cheb", h_levels=2):
+        """Jacobi(3,3) with omega = 2/3, or Cheb(3,3) = one degree-3
+        Chebyshev application before and after, on [lambda/4, lambda] with lambda from 10 Arnoldi
+        iterations; p-coarsening to 1, then `h_levels` geometric coarsenings."""
+        if smoother == "jacobi":
+            return MgParams(nu_pre=3, nu_post=3, smoother=1, lambda_method=1, h_levels=h_levels,
+                            eig_lo_frac=0.25, eig_hi_frac=1.0)
+        return MgParams(nu_pre=1, nu_post=1, cheb_degree=3, eig_lo_frac=0.25, eig_hi_frac=1.0, lambda_method=1,
+                        h_levels=h_levels)
 
     def _c(self):
         return _MgParams(self.nu_pre, self.nu_post, self.cheb_degree, self.eig_lo_frac, self.eig_hi_frac,
-                         self.power_iters, self.power_seed, self.coarse_rtol, self.coarse_max_iter)
+                         self.power_iters, self.power_seed, self.coarse_rtol, self.coarse_max_iter,
+                         self.smoother, self.jacobi_omega, self.lambda_method, self.h_levels)
 
 
 class Hierarchy:
