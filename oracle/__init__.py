@@ -78,6 +78,7 @@ def lib():
         L.orc_lambda_arnoldi.restype = d
         L.orc_jacobi.argtypes = [vp, vp, vp, i, d]
         L.orc_pair_kind.argtypes = [vp, vp]
+        L.orc_set_quadrature.argtypes = [i]
         L.orc_hier_create2.restype = vp
         L.orc_hier_create2.argtypes = [i, i, i, i, i, d, i, d, d, i, i, i, d, d, i, u64, d, i, i, i,
                                        i, d, i, i, C.POINTER(C.c_int)]
@@ -112,6 +113,12 @@ def _p(a):
 
 def set_threads(t: int):
     lib().orc_set_threads(int(t))
+
+
+def set_quadrature(q: int):
+    """0: LGL points collocated with the nodes (R1, default); 1: p+1 Gauss-Legendre points per
+    direction (NEXT-3).  Applies to levels / hierarchies created afterwards (oracle only)."""
+    lib().orc_set_quadrature(int(q))
 
 
 def get_threads() -> int:

@@ -108,22 +108,54 @@ double dlagrange(const std::vector<double>& xs, int m, double t) {
   return s;
 }
 
+// Gauss-Legendre points (roots of P_n) and weights 2 / ((1 - x^2) P_n'(x)^2), by Newton from
+// cos(pi (i + 3/4) / (n + 1/2)).  NEXT-3 ("Gauss quadrature").
+void gauss_legendre(int n, std::vector<double>& x, std::vector<double>& w) {
+  x.assign(n, 0.0); w.assign(n, 0.0);
+  for (int i = 0; i < n; ++i) {
+    double t = -std::cos(kPi * (i + 0.75) / (n + 0.5));
+    for (int it = 0; it < 100; ++it) {
+      double P, dP;
+      legendre(n, t, &P, &dP);
+      double dt = P / dP;
+      t -= dt;
+      if (std::fabs(dt) < 1e-16) break;
+    }
+    double P, dP;
+    legendre(n, t, &P, &dP);
+    x[i] = t;
+    w[i] = 2.0 / ((1.0 - t * t) * dP * dP);
+  }
+  for (int i = 0; i < n / 2; ++i) {   // symmetrise
+    double a = 0.5 * (x[n - 1 - i] - x[i]);
+    x[i] = -a; x[n - 1 - i] = a;
+    double ww = 0.5 * (w[i] + w[n - 1 - i]);
+    w[i] = w[n - 1 - i] = ww;
+  }
+  if (n % 2) x[n / 2] = 0.0;
+}
+
 struct Basis {
   int p = 0, n = 0;
-  std::vector<double> x, w;
-  std::vector<double> L;   // L[i*n+a]  = ell_a(xhat_i)   (tabulated, no delta shortcut)
-  std::vector<double> dL;  // dL[i*n+a] = ell_a'(xhat_i)  (the D matrix)
-  void build(int p_) {
-    p = p_; n = p + 1;
+  int quad = 0;             // 0: LGL points collocated with the nodes (R1); 1: n Gauss-Legendre points (NEXT-3)
+  std::vector<double> x, w;  // LGL nodes / weights
+  std::vector<double> qx, qw;   // quadrature points / weights
+  std::vector<double> L;   // L[i*n+a]  = ell_a(q_i)   (tabulated, no delta shortcut)
+  std::vector<double> dL;  // dL[i*n+a] = ell_a'(q_i)  (the D matrix when collocated)
+  void build(int p_, int quad_ = 0) {
+    p = p_; n = p + 1; quad = quad_;
     lgl(p, x, w);
+    if (quad == 1) gauss_legendre(n, qx, qw);
+    else { qx = x; qw = w; }
     L.assign(n * n, 0.0); dL.assign(n * n, 0.0);
     for (int i = 0; i < n; ++i)
       for (int a = 0; a < n; ++a) {
-        L[i * n + a] = lagrange(x, a, x[i]);
-        dL[i * n + a] = dlagrange(x, a, x[i]);
+        L[i * n + a] = lagrange(x, a, qx[i]);
+        dL[i * n + a] = dlagrange(x, a, qx[i]);
       }
   }
 };
+static int g_quad = 0;   // quadrature of levels created from now on (orc_set_quadrature)
 
 /* ------------------------------------------------------------------ seeded generator (R9, R15) */
 
@@ -233,6 +265,17 @@ inline void grad_phi(const Basis& B, int i, int j, int k, int a, int b, int c, d
   d[0] = dLa * Lb * Lc; d[1] = La * dLb * Lc; d[2] = La * Lb * dLc;
 }
 
+// Physical position of quadrature point (i,j,k): x(xi_q) = sum_l x_l phi_l(xi_q) (isoparametric map).
+inline void quad_point(const Level& L, const std::vector<double>& X, int i, int j, int k, double xq[3]) {
+  int n = L.n; int64_t n3 = L.n3;
+  xq[0] = xq[1] = xq[2] = 0.0;
+  for (int c = 0; c < n; ++c) for (int b = 0; b < n; ++b) for (int a = 0; a < n; ++a) {
+    int64_t l = a + n * (b + n * c);
+    double ph = L.B.L[i * n + a] * L.B.L[j * n + b] * L.B.L[k * n + c];
+    xq[0] += ph * X[l]; xq[1] += ph * X[n3 + l]; xq[2] += ph * X[2 * n3 + l];
+  }
+}
+
 // Isoparametric geometric factors of one element (R1, R2, R3):
 // G_q = w_i w_j w_k mu(x_q) detJ_q J_q^{-1} J_q^{-T}, J[al][be] = d x_al / d xi_be.
 // Returns min det J over the element.
@@ -278,8 +321,10 @@ double element_geometry(const Level& L, int64_t e, double* G, double* dJ, int ge
         Ji[2][0] = (J[1][0] * J[2][1] - J[1][1] * J[2][0]) / det;
         Ji[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) / det;
         Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) / det;
-        double mu = coeff_mu(L.coeff, L.c0, L.c1, X[q], X[n3 + q], X[2 * n3 + q]);
-        double s = L.B.w[i] * L.B.w[j] * L.B.w[k] * mu * det;
+        double xq[3] = {X[q], X[n3 + q], X[2 * n3 + q]};   // collocated: the node itself
+        if (L.B.quad == 1) quad_point(L, X, i, j, k, xq);
+        double mu = coeff_mu(L.coeff, L.c0, L.c1, xq[0], xq[1], xq[2]);
+        double s = L.B.qw[i] * L.B.qw[j] * L.B.qw[k] * mu * det;
         double M[3][3];
         for (int al = 0; al < 3; ++al)
           for (int be = 0; be < 3; ++be) {
@@ -434,7 +479,7 @@ void apply(const Level& L, int bc, const double* u, double* v, int tier) {
         for (int c = 0; c < n; ++c) for (int b = 0; b < n; ++b) for (int a = 0; a < n; ++a)
           ue[a + n * (b + n * c)] = um[L.l2g(e, a, b, c)];
         const double* G = elem_G(L, e, gbuf);
-        if (tier == 2) element_apply_o2(L, G, ue.data(), ve.data());
+        if (tier == 2 || L.B.quad == 1) element_apply_o2(L, G, ue.data(), ve.data());
         else element_apply_o3(L, G, ue.data(), ve.data());
         for (int c = 0; c < n; ++c) for (int b = 0; b < n; ++b) for (int a = 0; a < n; ++a)
           v[L.l2g(e, a, b, c)] += ve[a + n * (b + n * c)];
@@ -834,6 +879,9 @@ int vcycle(Hier& H, int l, const double* b, double* x) {
 extern "C" {
 
 void orc_set_threads(int t) { if (t > 0) omp_set_num_threads(t); }
+// Quadrature of levels created afterwards: 0 collocated LGL (R1, default), 1 Gauss-Legendre with
+// p + 1 points per direction (NEXT-3).  Oracle-only: the GPU path is collocated.
+void orc_set_quadrature(int q) { g_quad = (q == 1) ? 1 : 0; }
 int orc_get_threads(void) { return omp_get_max_threads(); }
 
 int orc_lgl(int p, double* x, double* w) {
@@ -890,7 +938,8 @@ void* orc_level_create(int nex, int ney, int nez, int p, int warp, double amp, i
   L->N = L->Mx * L->My * L->Mz;
   L->n3 = (int64_t)L->n * L->n * L->n;
   L->geom_tier = geom_tier; L->tier = tier; L->eager = eager != 0;
-  L->B.build(p);
+  L->B.build(p, g_quad);
+  if (g_quad == 1) { L->geom_tier = 2; L->tier = 2; }   // O3 / factorised J assume collocation
   L->colour_elems.assign(8, {});
   for (int64_t e = 0; e < L->E; ++e) {
     int ex, ey, ez; L->elem_coords(e, ex, ey, ez);
@@ -1196,7 +1245,9 @@ int orc_load_vector(void* h, int rhs_id, double* f) {
         element_nodes(*L, e, X);
         for (int c = 0; c < n; ++c) for (int b = 0; b < n; ++b) for (int a = 0; a < n; ++a) {
           int64_t q = a + n * (b + n * c);
-          double x = X[q], y = X[n3 + q], z = X[2 * n3 + q];
+          double xq[3] = {X[q], X[n3 + q], X[2 * n3 + q]};
+          if (L->B.quad == 1) quad_point(*L, X, a, b, c, xq);
+          double x = xq[0], y = xq[1], z = xq[2];
           double us = std::sin(kPi * x) * std::sin(kPi * y) * std::sin(kPi * z);
           double gu[3] = {kPi * std::cos(kPi * x) * std::sin(kPi * y) * std::sin(kPi * z),
                           kPi * std::sin(kPi * x) * std::cos(kPi * y) * std::sin(kPi * z),
@@ -1205,7 +1256,10 @@ int orc_load_vector(void* h, int rhs_id, double* f) {
           coeff_grad(L->coeff, L->c0, L->c1, x, y, z, gm);
           double mu = coeff_mu(L->coeff, L->c0, L->c1, x, y, z);
           double fx = 3.0 * kPi * kPi * mu * us - (gm[0] * gu[0] + gm[1] * gu[1] + gm[2] * gu[2]);
-          f[L->l2g(e, a, b, c)] += L->B.w[a] * L->B.w[b] * L->B.w[c] * dJ[q] * fx;
+          const double wq = L->B.qw[a] * L->B.qw[b] * L->B.qw[c] * dJ[q] * fx;
+          if (L->B.quad == 0) { f[L->l2g(e, a, b, c)] += wq; continue; }
+          for (int cc = 0; cc < n; ++cc) for (int bb = 0; bb < n; ++bb) for (int aa = 0; aa < n; ++aa)   // phi_l(x_q)
+            f[L->l2g(e, aa, bb, cc)] += L->B.L[a * n + aa] * L->B.L[b * n + bb] * L->B.L[c * n + cc] * wq;
         }
       }
     }

@@ -129,3 +129,25 @@ def test_paper_hierarchy_invalid(S):
     with pytest.raises(S.SfmgError) as ex:
         S.Hierarchy(S.Problem.from_dict(inputs.problem(6, 2)), S.MgParams.paper("cheb", h_levels=2))
     assert ex.value.status == "SFMG_E_PCOARSEN"
+
+
+def test_3dconst_paper_settings_against_golden(S):
+    """tab:3d-box setting (3d-const, 8^3, p = 2..16, paper hierarchy and smoothers; NEXT-1): GPU iteration
+    counts +-1 of the oracle's (tests/golden/next1_3dconst_oracle.json, written from oracle/ only)."""
+    import torch
+    g = json.load(open(os.path.join(GOLDEN, "next1_3dconst_oracle.json")))
+    for p in (2, 4, 8, 16):
+        d = inputs.problem(8, p)   # unit cube, mu = 1 (P:892-893)
+        for name in ("jacobi33", "cheb33"):
+            H = S.Hierarchy(S.Problem.from_dict(d), S.MgParams.paper("jacobi" if name == "jacobi33" else "cheb", 2))
+            b = H.levels[0].load_vector(1)
+            for mode, mname in ((0, "mg_solver"), (1, "pcg")):
+                ref = g["runs"]["p%d_%s_%s" % (p, mname, name)]
+                for l, lam in enumerate(ref["lambda"]):
+                    assert abs(H.lam(l) - lam) <= 1e-9 * lam, (p, name, l)
+                _, rep = H.solve(b, mode=mode, rtol=1e-8, max_iter=300)
+                assert rep["converged"] == ref["converged"]
+                assert abs(rep["iterations"] - ref["iterations"]) <= 1, (p, name, mname, rep["iterations"])
+                assert rep["r_norm"] <= 1e-8 * rep["r0_norm"]
+            del H
+            torch.cuda.empty_cache()
