@@ -414,6 +414,26 @@ def run_extras(args, sfmg, dev, stream, flush, hbm_peak):
     out["config5_pmg_pcg"] = {"N": H.N, "levels": H.nlevels, "setup_s": t_setup, "pcg_iterations": rep["iterations"],
                               "converged": rep["converged"], "rel_residual": rep["r_norm"] / rep["r0_norm"],
                               "solve_ms": t_solve * 1e3, "vcycle_ms": tv * 1e3, "fine_applies": rep["fine_applies"]}
+    del H
+    # NEXT-1: the paper's own settings on its 3d-const problem (8^3, p = 16, unit cube, mu = 1):
+    # Jacobi(3,3) / Cheb(3,3) on [lambda/4, lambda] (10 Arnoldi), p -> 1 then 8^3 -> 4^3 -> 2^3
+    d = inputs.problem(8, 16)
+    nx = {}
+    for sm in ("jacobi", "cheb"):
+        H = sfmg.Hierarchy(sfmg.Problem.from_dict(d), sfmg.MgParams.paper(sm, h_levels=2), device=dev)
+        bvec = H.levels[0].load_vector(1)
+        for mode, mname in ((0, "mg_solver"), (1, "pcg")):
+            H.solve(bvec, mode=mode, rtol=1e-8, max_iter=300)
+            torch.cuda.synchronize()
+            a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            _, rep = H.solve(bvec, mode=mode, rtol=1e-8, max_iter=300)
+            e.record(stream)
+            e.synchronize()
+            nx["%s_%s33" % (mname, sm)] = {"iterations": rep["iterations"], "converged": rep["converged"],
+                                            "solve_ms": a.elapsed_time(e), "fine_applies": rep["fine_applies"]}
+        del H
+    out["next1_3dconst_p16_paper_settings"] = nx
     return out
 
 
