@@ -371,6 +371,9 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
   using C = V4Cfg<P, GS>;
   constexpr int N = C::N, N2 = C::N2, N3 = C::N3;
   constexpr bool EO = (P % 2 == 0) && P >= 4;   // even-odd line products
+  // the next group's u column is loaded right after this group's is staged, so it is in flight
+  // during the whole element (measured: p = 16 -2.5 %, p <= 8 within noise)
+  constexpr bool EARLY = true;
   extern __shared__ __align__(128) double smem[];
   double* sG = smem;                                   // [EPB][k][6][n^2] (GS)
   const int le = threadIdx.x / N2;
@@ -460,6 +463,11 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
     }
 #pragma unroll
     for (int k = 0; k < N; ++k) su[t + N2 * k] = ru[k];
+    double rn[N];
+    if (EARLY && grp + gstride < ngroups) {   // next group's u column, in flight during the whole element
+      load_column(grp + gstride, rn);
+      if (grp + 2 * gstride < ngroups) prefetch_column(grp + 2 * gstride);
+    }
     __syncthreads();
     {  // P1: g0 on x-line (j=t0, k=t1) -> s0
       double L[N];
@@ -562,8 +570,7 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
         if (nx + gstride < ngroups) prefetch_group_l2(nx + gstride);
       }
     }
-    double rn[N];   // next group's u column, in flight during P4-P6
-    if (grp + gstride < ngroups) {
+    if (!EARLY && grp + gstride < ngroups) {   // next group's u column, in flight during P4-P6
       load_column(grp + gstride, rn);
       if (grp + 2 * gstride < ngroups) prefetch_column(grp + 2 * gstride);
     }
