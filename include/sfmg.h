@@ -134,7 +134,8 @@ sfmg_status sfmg_apply(sfmg_level lv, int32_t bc, const double* d_u, double* d_v
 /* diag(A_D) (bc = 0: boundary entries 1) or diag(A) (bc = 1). */
 sfmg_status sfmg_diag(sfmg_level lv, int32_t bc, double* d_diag, int64_t n, void* stream);
 /* lambda_max of D^{-1} A_D by `iters` power iterations with the D-Rayleigh quotient from a
- * splitmix64(seed) start vector, boundary zeroed (R9).  Syncs. */
+ * splitmix64(seed) start vector, boundary zeroed (R9).  Syncs.
+ * SFMG_E_ARG on a level without interior dofs (the start vector would be zero). */
 sfmg_status sfmg_lambda_max(sfmg_level lv, int32_t iters, uint64_t seed, double* h_lambda,
                             void* stream);
 /* lambda_max of D^{-1} A_D by `steps` Arnoldi iterations in the D-inner product <x,y>_D =

@@ -386,6 +386,10 @@ sfmg_status sfmg_diag(sfmg_level lv, int32_t bc, double* d_diag, int64_t n, void
 
 sfmg_status sfmg_lambda_max(sfmg_level lv, int32_t iters, uint64_t seed, double* h_lambda, void* stream) {
   if (!lv || !h_lambda || iters < 1) return SFMG_E_ARG;
+  if ((long long)(lv->m.Mx - 2) * (lv->m.My - 2) * (lv->m.Mz - 2) <= 0) {
+    set_error("level has no interior dofs: D^{-1} A_D is the identity on the boundary");
+    return SFMG_E_ARG;
+  }
   cudaStream_t s = (cudaStream_t)stream;
   double* x = lv->t1;
   double* y = lv->y;

@@ -220,3 +220,39 @@ def test_vcycle_and_solves_small(S, orc):
         assert rg["r_norm"] <= 1e-8 * rg["r0_norm"]
         assert rg["fine_applies"] == ro["fine_applies"] or abs(rg["iterations"] - ro["iterations"]) == 1
         assert rel_err(xg.cpu().numpy(), ro["x"], np.abs(ro["x"]).max()) <= 1e-6
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 5, 8, 16])
+def test_degenerate_and_bc1_cases(S, orc, p):
+    """Edge cases: a single element (p = 1: no interior dof at all, A_D = I), the un-projected operator
+    (bc = 1) against the oracle and its any-size property A 1 = 0, and a zero right-hand side."""
+    import torch
+    d = inputs.problem(1, p, **WARP)
+    g = gpu_level(S, d)
+    o = orc_level(orc, d, tier=3, geom_tier=3)
+    u = inputs.uniform_pm1(3, g.N)
+    for bc in (0, 1):
+        ref = o.apply(u, bc, tier=3)
+        got = g.apply(to_gpu(u), bc=bc).cpu().numpy()
+        assert rel_err(got, ref, np.abs(ref).max()) <= 1e-11, (p, bc)
+    if p == 1:
+        np.testing.assert_array_equal(g.apply(to_gpu(u)).cpu().numpy(), u)   # every node is a boundary node
+        with pytest.raises(S.SfmgError):
+            g.lambda_max(10, 12345)
+    # A 1 = 0 without the boundary projection, on a warped multi-element mesh
+    d2 = inputs.problem(2, p, ney=1, nez=2, **WARP)
+    g2 = gpu_level(S, d2)
+    ones = torch.ones(g2.N, dtype=torch.float64, device="cuda")
+    r = g2.apply(ones, bc=1).cpu().numpy()
+    dg = g2.diag(bc=1).cpu().numpy()
+    assert np.abs(r).max() <= 1e-12 * np.abs(dg).max(), p
+
+
+def test_zero_rhs_solve(S):
+    import torch
+    H = S.Hierarchy(S.Problem.from_dict(inputs.problem(2, 4, **WARP)), S.MgParams())
+    b = torch.zeros(H.N, dtype=torch.float64, device="cuda")
+    for mode in (0, 1):
+        x, rep = H.solve(b, mode=mode)
+        assert rep["converged"] and rep["iterations"] == 0
+        assert float(x.abs().max()) == 0.0
