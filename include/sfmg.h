@@ -58,6 +58,10 @@ typedef struct {
   double warp_amp;         /*   (reference-cube point mapped per component; boundary fixed)  */
   int32_t coeff;           /* mu at the physical nodes: 0: c0; 1: exp(c1 S); 2: 10^(c1 S);   */
   double c0, c1;           /*   3: c0 + c1 sum_i cos^2(2 pi x_i); S = sin2pix sin2piy sin2piz */
+  int32_t quadrature;      /* 0: (p+1)^3 LGL points collocated with the nodes (R1, BASELINE);  */
+                           /* 1: (p+1)^3 Gauss-Legendre points, nodal LGL basis ("Gauss   */
+                           /*    quadrature"): G is stored at the Gauss     */
+                           /*    points and the apply adds interpolation passes               */
 } sfmg_problem;
 
 /* p-multigrid parameters (R7-R11, R13).  The last four fields select

@@ -12,7 +12,7 @@ CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 BUILD = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "libsfmg.so")
-SOURCES = ["basis.cu", "k_operator.cu", "k_blas.cu", "k_transfer.cu", "sfmg_api.cu"]
+SOURCES = ["basis.cu", "k_operator.cu", "k_gauss.cu", "k_blas.cu", "k_transfer.cu", "sfmg_api.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
@@ -28,8 +28,8 @@ def _stale(out: str, deps) -> bool:
 
 def _compile(src: str) -> str:
     obj = os.path.join(BUILD, os.path.splitext(src)[0] + ".o")
-    deps = [os.path.join(CSRC, src), os.path.join(CSRC, "sfmg_internal.h"), os.path.join(INCLUDE, "sfmg.h"),
-            __file__]
+    deps = [os.path.join(CSRC, src), os.path.join(CSRC, "sfmg_internal.h"), os.path.join(CSRC, "k_common.cuh"),
+            os.path.join(INCLUDE, "sfmg.h"), __file__]
     if _stale(obj, deps):
         log = obj + ".log"
         cmd = [NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]

@@ -1,0 +1,770 @@
+// Gauss-Legendre quadrature variant of the operator ("The Jacobians for
+// this transformation are computed at every quadrature point, and Gauss quadrature is used to
+// numerically approximate integrals").  The basis stays the nodal LGL basis of order p; the
+// quadrature uses n = p + 1 Gauss-Legendre points per direction (exact for degree 2p + 1, so the
+// stiffness of affine elements is integrated exactly).  Tables (host, per order):
+//   B[i][a]  = ell_a(xi_i)     nodal basis at the Gauss points          (interpolation)
+//   DB[i][a] = ell_a'(xi_i)    its derivative (geometry)
+//   DG[i][m] = ell^G_m'(xi_i)  derivative matrix of the Lagrange basis on the Gauss points
+// Apply per element (same structure as the collocated operator on the Gauss grid, wrapped in
+// interpolations): u_q = (B x B x B) u_e; g = (DG x I x I, I x DG x I, I x I x DG) u_q (exact: u_q
+// represents the same degree-p polynomial); w = G_q g; v_q = DG^T contractions of w;
+// v_e = (B^T x B^T x B^T) v_q; scatter.  G_q = wG_i wG_j wG_k mu(x(xi_q)) detJ_q J_q^{-1} J_q^{-T}
+// with J and x from the isoparametric map evaluated at the Gauss points.
+#include <cmath>
+
+#include "k_common.cuh"
+
+namespace sfmg {
+
+constexpr int qOffset(int P) {
+  int s = 0;
+  for (int q = 1; q < P; ++q) s += (q + 1) * (q + 1);
+  return s;
+}
+constexpr int qvOffset(int P) {
+  int s = 0;
+  for (int q = 1; q < P; ++q) s += q + 1;
+  return s;
+}
+__constant__ double c_qB[qOffset(kMaxOrder + 1)];
+__constant__ double c_qDB[qOffset(kMaxOrder + 1)];
+__constant__ double c_qDG[qOffset(kMaxOrder + 1)];
+__constant__ double c_qw[qvOffset(kMaxOrder + 1)];   // Gauss weights
+__constant__ double c_qxn[qvOffset(kMaxOrder + 1)];  // LGL nodes (node positions)
+
+// ---------------------------------------------------------------------------- host tables
+
+// Gauss-Legendre points (roots of P_n) and weights 2 / ((1 - x^2) P_n'(x)^2): Newton's method on
+// the three-term recurrence from the Chebyshev-like guesses cos(pi (i + 3/4) / (n + 1/2)).
+static void gauss_rule(int n, std::vector<double>& x, std::vector<double>& w) {
+  x.resize(n);
+  w.resize(n);
+  for (int i = 0; i < n; ++i) {
+    double t = std::cos(M_PI * (n - 1 - i + 0.75) / (n + 0.5));   // ascending order
+    double dp = 1.0;
+    for (int it = 0; it < 100; ++it) {
+      double p0 = 1.0, p1 = t;
+      for (int k = 2; k <= n; ++k) {
+        const double p2 = ((2.0 * k - 1.0) * t * p1 - (k - 1.0) * p0) / k;
+        p0 = p1;
+        p1 = p2;
+      }
+      const double pn = (n == 0) ? 1.0 : p1, pm = (n == 0) ? 0.0 : p0;
+      dp = n * (t * pn - pm) / (t * t - 1.0);
+      const double dt = pn / dp;
+      t -= dt;
+      if (std::fabs(dt) < 1e-16) break;
+    }
+    double p0 = 1.0, p1 = t;
+    for (int k = 2; k <= n; ++k) {
+      const double p2 = ((2.0 * k - 1.0) * t * p1 - (k - 1.0) * p0) / k;
+      p0 = p1;
+      p1 = p2;
+    }
+    dp = n * (t * p1 - p0) / (t * t - 1.0);
+    x[i] = t;
+    w[i] = 2.0 / ((1.0 - t * t) * dp * dp);
+  }
+  for (int i = 0; i < n / 2; ++i) {   // exact symmetry
+    const double a = 0.5 * (x[n - 1 - i] - x[i]), b = 0.5 * (w[i] + w[n - 1 - i]);
+    x[i] = -a;
+    x[n - 1 - i] = a;
+    w[i] = w[n - 1 - i] = b;
+  }
+  if (n % 2) x[n / 2] = 0.0;
+}
+
+// Lagrange cardinal ell_a on nodes xs at t (barycentric weights), and its derivative.
+static double lag_val(const std::vector<double>& xs, int a, double t) {
+  double v = 1.0;
+  for (size_t k = 0; k < xs.size(); ++k)
+    if ((int)k != a) v *= (t - xs[k]) / (xs[a] - xs[k]);
+  return v;
+}
+static double lag_der(const std::vector<double>& xs, int a, double t) {
+  double s = 0.0;
+  for (size_t j = 0; j < xs.size(); ++j) {
+    if ((int)j == a) continue;
+    double v = 1.0 / (xs[a] - xs[j]);
+    for (size_t k = 0; k < xs.size(); ++k)
+      if ((int)k != a && k != j) v *= (t - xs[k]) / (xs[a] - xs[k]);
+    s += v;
+  }
+  return s;
+}
+
+static bool g_gauss_uploaded[kMaxOrder + 1];
+
+cudaError_t upload_gauss_tables(int p) {
+  if (p < 1 || p > kMaxOrder) return cudaErrorInvalidValue;
+  if (g_gauss_uploaded[p]) return cudaSuccess;
+  const int n = p + 1;
+  Basis1D L = make_basis(p);
+  std::vector<double> gx, gw;
+  gauss_rule(n, gx, gw);
+  std::vector<double> B(n * n), DB(n * n), DG(n * n);
+  for (int i = 0; i < n; ++i)
+    for (int a = 0; a < n; ++a) {
+      B[i * n + a] = lag_val(L.x, a, gx[i]);
+      DB[i * n + a] = lag_der(L.x, a, gx[i]);
+      DG[i * n + a] = lag_der(gx, a, gx[i]);
+    }
+  const size_t mo = sizeof(double) * qOffset(p), vo = sizeof(double) * qvOffset(p);
+  cudaError_t e;
+  if ((e = cudaMemcpyToSymbol(c_qB, B.data(), sizeof(double) * n * n, mo))) return e;
+  if ((e = cudaMemcpyToSymbol(c_qDB, DB.data(), sizeof(double) * n * n, mo))) return e;
+  if ((e = cudaMemcpyToSymbol(c_qDG, DG.data(), sizeof(double) * n * n, mo))) return e;
+  if ((e = cudaMemcpyToSymbol(c_qw, gw.data(), sizeof(double) * n, vo))) return e;
+  if ((e = cudaMemcpyToSymbol(c_qxn, L.x.data(), sizeof(double) * n, vo))) return e;
+  g_gauss_uploaded[p] = true;
+  return cudaSuccess;
+}
+
+template <int P> __device__ __forceinline__ double qB(int i, int a) { return c_qB[qOffset(P) + i * (P + 1) + a]; }
+template <int P> __device__ __forceinline__ double qDG(int i, int a) { return c_qDG[qOffset(P) + i * (P + 1) + a]; }
+
+// Element geometry at the Gauss points into smem tables: per point J (9), x (3), from the nodal
+// positions X[3][n^3] (smem) and the B / DB tables (smem copies sB, sDB).
+template <int P>
+__device__ __forceinline__ void gauss_jacobian(const double* X, const double* sB, const double* sDB, int i, int j, int k,
+                                               double J[3][3], double xq[3]) {
+  constexpr int N = P + 1, N3 = N * N * N;
+#pragma unroll
+  for (int al = 0; al < 3; ++al) { J[al][0] = J[al][1] = J[al][2] = 0.0; xq[al] = 0.0; }
+  for (int c = 0; c < N; ++c) {
+    const double Bk = sB[k * N + c], Dk = sDB[k * N + c];
+    for (int b = 0; b < N; ++b) {
+      const double Bj = sB[j * N + b], Dj = sDB[j * N + b];
+      const double bjk = Bj * Bk, djk = Dj * Bk, bjdk = Bj * Dk;
+      for (int a = 0; a < N; ++a) {
+        const double Bi = sB[i * N + a], Di = sDB[i * N + a];
+        const int l = a + N * (b + N * c);
+        const double p0 = Di * bjk, p1 = Bi * djk, p2 = Bi * bjdk, ph = Bi * bjk;
+#pragma unroll
+        for (int al = 0; al < 3; ++al) {
+          const double x = X[al * N3 + l];
+          J[al][0] = fma(x, p0, J[al][0]);
+          J[al][1] = fma(x, p1, J[al][1]);
+          J[al][2] = fma(x, p2, J[al][2]);
+          xq[al] = fma(x, ph, xq[al]);
+        }
+      }
+    }
+  }
+}
+
+template <int P>
+__device__ __forceinline__ void load_tables_and_nodes(const MeshDev& m, long long e, double* X, double* sB, double* sDB) {
+  constexpr int N = P + 1, N2 = N * N, N3 = N2 * N;
+  for (int t = threadIdx.x; t < N2; t += blockDim.x) {
+    sB[t] = c_qB[qOffset(P) + t];
+    sDB[t] = c_qDB[qOffset(P) + t];
+  }
+  int ex, ey, ez;
+  elem_coords(m, e, ex, ey, ez);
+  const double* xn = c_qxn + qvOffset(P);
+  for (int l = threadIdx.x; l < N3; l += blockDim.x) {
+    const int a = l % N, b = (l / N) % N, c = l / N2;
+    double x[3];
+    node_pos<P>(m, xn, ex, ey, ez, a, b, c, x);
+    X[l] = x[0];
+    X[N3 + l] = x[1];
+    X[2 * N3 + l] = x[2];
+  }
+}
+
+// ---------------------------------------------------------------------------- geometry
+
+template <int P>
+__global__ void __launch_bounds__(256) k_geometry_gauss(MeshDev m, double* __restrict__ G, int* bad) {
+  constexpr int N = P + 1, N2 = N * N, N3 = N2 * N;
+  extern __shared__ double gsm[];
+  double* X = gsm;              // [3][N3]
+  double* sB = X + 3 * N3;      // [N2]
+  double* sDB = sB + N2;        // [N2]
+  const double* w = c_qw + qvOffset(P);
+  for (long long e = blockIdx.x; e < m.E; e += gridDim.x) {
+    __syncthreads();
+    load_tables_and_nodes<P>(m, e, X, sB, sDB);
+    __syncthreads();
+    for (int q = threadIdx.x; q < N3; q += blockDim.x) {
+      const int i = q % N, j = (q / N) % N, k = q / N2;
+      double J[3][3], xq[3];
+      gauss_jacobian<P>(X, sB, sDB, i, j, k, J, xq);
+      const double det = J[0][0] * (J[1][1] * J[2][2] - J[1][2] * J[2][1]) -
+                         J[0][1] * (J[1][0] * J[2][2] - J[1][2] * J[2][0]) +
+                         J[0][2] * (J[1][0] * J[2][1] - J[1][1] * J[2][0]);
+      if (!(det > 0.0)) atomicAdd(bad, 1);
+      const double id = 1.0 / det;
+      double Ji[3][3];
+      Ji[0][0] = (J[1][1] * J[2][2] - J[1][2] * J[2][1]) * id;
+      Ji[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) * id;
+      Ji[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) * id;
+      Ji[1][0] = (J[1][2] * J[2][0] - J[1][0] * J[2][2]) * id;
+      Ji[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) * id;
+      Ji[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * id;
+      Ji[2][0] = (J[1][0] * J[2][1] - J[1][1] * J[2][0]) * id;
+      Ji[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) * id;
+      Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * id;
+      const double s = w[i] * w[j] * w[k] * coeff_mu(m, xq[0], xq[1], xq[2]) * det;
+      const int comp[6][2] = {{0, 0}, {0, 1}, {0, 2}, {1, 1}, {1, 2}, {2, 2}};
+#pragma unroll
+      for (int c = 0; c < 6; ++c) {
+        const int a = comp[c][0], b = comp[c][1];
+        G[GLayout<P>::off(e, c, i + N * j, k)] = s * (Ji[a][0] * Ji[b][0] + Ji[a][1] * Ji[b][1] + Ji[a][2] * Ji[b][2]);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------- apply
+
+// out = M L on one line, M[i][m] = B (T = false) or its transpose (T = true), DG likewise.
+template <int P, bool T>
+__device__ __forceinline__ void line_B(const double (&L)[P + 1], double (&out)[P + 1]) {
+  constexpr int N = P + 1;
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    double s = 0.0;
+#pragma unroll
+    for (int m = 0; m < N; ++m) s = fma(T ? qB<P>(m, i) : qB<P>(i, m), L[m], s);
+    out[i] = s;
+  }
+}
+template <int P, bool T>
+__device__ __forceinline__ void line_DG(const double (&L)[P + 1], double (&out)[P + 1]) {
+  constexpr int N = P + 1;
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    double s = 0.0;
+#pragma unroll
+    for (int m = 0; m < N; ++m) s = fma(T ? qDG<P>(m, i) : qDG<P>(i, m), L[m], s);
+    out[i] = s;
+  }
+}
+
+template <int P>
+struct GaussCfg {
+  static constexpr int N = P + 1, N2 = N * N, N3 = N2 * N;
+  static constexpr int EPB = 128 / N2 > 0 ? 128 / N2 : 1;
+  static constexpr int THREADS = EPB * N2;
+  static constexpr size_t SMEM = sizeof(double) * 3 * N3 * EPB;
+};
+
+// Block = EPB elements x n^2 threads; thread (t0, t1) owns one line per pass (see file header).
+template <int P, bool DIR>
+__global__ void __launch_bounds__(GaussCfg<P>::THREADS) k_apply_gauss(MeshDev m, const double* __restrict__ G,
+                                                                      const double* __restrict__ u,
+                                                                      double* __restrict__ v) {
+  using C = GaussCfg<P>;
+  constexpr int N = C::N, N2 = C::N2, N3 = C::N3;
+  extern __shared__ double asm_[];
+  const int le = threadIdx.x / N2, t = threadIdx.x - le * N2, t0 = t % N, t1 = t / N;
+  double* A = asm_ + le * 3 * N3;
+  double* Bb = A + N3;
+  double* Cc = Bb + N3;
+  const long long sxy = (long long)m.Mx * m.My;
+  const long long ngroups = (m.E + C::EPB - 1) / C::EPB;
+  for (long long grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+    const long long e = grp * C::EPB + le;
+    const bool act = e < m.E;
+    int ex = 0, ey = 0, ez = 0;
+    if (act) elem_coords(m, e, ex, ey, ez);
+    __syncthreads();
+    {  // gather: nodal column (a = t0, b = t1), masked (R4)
+      const int I = ex * P + t0, J = ey * P + t1;
+      const long long col = (long long)I + (long long)m.Mx * J + sxy * (long long)(ez * P);
+#pragma unroll
+      for (int c = 0; c < N; ++c) {
+        const int K = ez * P + c;
+        const bool bnd = DIR && (I == 0 || I == m.Mx - 1 || J == 0 || J == m.My - 1 || K == 0 || K == m.Mz - 1);
+        A[t0 + N * t1 + N2 * c] = (act && !bnd) ? __ldg(u + col + sxy * c) : 0.0;
+      }
+    }
+    __syncthreads();
+    {  // x-interpolation: line (b = t0, c = t1)
+      double L[N], o[N];
+#pragma unroll
+      for (int a = 0; a < N; ++a) L[a] = A[a + N * t0 + N2 * t1];
+      line_B<P, false>(L, o);
+#pragma unroll
+      for (int i = 0; i < N; ++i) Bb[i + N * t0 + N2 * t1] = o[i];
+    }
+    __syncthreads();
+    {  // y-interpolation: line (i = t0, c = t1)
+      double L[N], o[N];
+#pragma unroll
+      for (int b = 0; b < N; ++b) L[b] = Bb[t0 + N * b + N2 * t1];
+      line_B<P, false>(L, o);
+#pragma unroll
+      for (int j = 0; j < N; ++j) A[t0 + N * j + N2 * t1] = o[j];
+    }
+    __syncthreads();
+    double g2[N];
+    {  // z-interpolation and z-gradient in registers: column (i = t0, j = t1)
+      double L[N], uq[N];
+#pragma unroll
+      for (int c = 0; c < N; ++c) L[c] = A[t0 + N * t1 + N2 * c];
+      line_B<P, false>(L, uq);
+      line_DG<P, false>(uq, g2);
+#pragma unroll
+      for (int k = 0; k < N; ++k) Cc[t0 + N * t1 + N2 * k] = uq[k];
+    }
+    __syncthreads();
+    {  // x- and y-gradients on the Gauss grid: lines (j = t0, k = t1) -> A, (i = t0, k = t1) -> Bb
+      double L[N], o[N], L2[N], o2[N];
+#pragma unroll
+      for (int mm = 0; mm < N; ++mm) {
+        L[mm] = Cc[mm + N * t0 + N2 * t1];
+        L2[mm] = Cc[t0 + N * mm + N2 * t1];
+      }
+      line_DG<P, false>(L, o);
+      line_DG<P, false>(L2, o2);
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        A[i + N * t0 + N2 * t1] = o[i];
+        Bb[t0 + N * i + N2 * t1] = o2[i];
+      }
+    }
+    __syncthreads();
+    double vz[N];
+    {  // pointwise w = G g (G at the Gauss points), then D_G^T along z: column (i = t0, j = t1)
+      double w2[N];
+      const long long eg = act ? e : 0;
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        const int idx = t0 + N * t1 + N2 * k, ij = t0 + N * t1;
+        const double G00 = __ldg(G + GLayout<P>::off(eg, 0, ij, k)), G01 = __ldg(G + GLayout<P>::off(eg, 1, ij, k));
+        const double G02 = __ldg(G + GLayout<P>::off(eg, 2, ij, k)), G11 = __ldg(G + GLayout<P>::off(eg, 3, ij, k));
+        const double G12 = __ldg(G + GLayout<P>::off(eg, 4, ij, k)), G22 = __ldg(G + GLayout<P>::off(eg, 5, ij, k));
+        const double a0 = A[idx], a1 = Bb[idx], a2 = g2[k];
+        A[idx] = G00 * a0 + G01 * a1 + G02 * a2;
+        Bb[idx] = G01 * a0 + G11 * a1 + G12 * a2;
+        w2[k] = G02 * a0 + G12 * a1 + G22 * a2;
+      }
+      line_DG<P, true>(w2, vz);
+    }
+    __syncthreads();
+    {  // D_G^T on x-lines of A (in place) and y-lines of Bb (in place)
+      double L[N], o[N], L2[N], o2[N];
+#pragma unroll
+      for (int mm = 0; mm < N; ++mm) {
+        L[mm] = A[mm + N * t0 + N2 * t1];
+        L2[mm] = Bb[t0 + N * mm + N2 * t1];
+      }
+      line_DG<P, true>(L, o);
+      line_DG<P, true>(L2, o2);
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        A[i + N * t0 + N2 * t1] = o[i];
+        Bb[t0 + N * i + N2 * t1] = o2[i];
+      }
+    }
+    __syncthreads();
+    {  // v_q, then B^T along z: column (i = t0, j = t1) -> Cc (nodal c)
+      double vq[N], o[N];
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        const int idx = t0 + N * t1 + N2 * k;
+        vq[k] = A[idx] + Bb[idx] + vz[k];
+      }
+      line_B<P, true>(vq, o);
+#pragma unroll
+      for (int c = 0; c < N; ++c) Cc[t0 + N * t1 + N2 * c] = o[c];
+    }
+    __syncthreads();
+    {  // B^T along y: line (i = t0, c = t1) -> A (nodal b)
+      double L[N], o[N];
+#pragma unroll
+      for (int j = 0; j < N; ++j) L[j] = Cc[t0 + N * j + N2 * t1];
+      line_B<P, true>(L, o);
+#pragma unroll
+      for (int b = 0; b < N; ++b) A[t0 + N * b + N2 * t1] = o[b];
+    }
+    __syncthreads();
+    if (act) {  // B^T along x: line (b = t0, c = t1) -> nodal a, scatter (fp64 RED)
+      double L[N], o[N];
+#pragma unroll
+      for (int i = 0; i < N; ++i) L[i] = A[i + N * t0 + N2 * t1];
+      line_B<P, true>(L, o);
+      const int J = ey * P + t0, K = ez * P + t1;
+      const long long row = (long long)m.Mx * J + sxy * K + (long long)ex * P;
+#pragma unroll
+      for (int a = 0; a < N; ++a) {
+        const int I = ex * P + a;
+        const bool bnd = DIR && (I == 0 || I == m.Mx - 1 || J == 0 || J == m.My - 1 || K == 0 || K == m.Mz - 1);
+        if (!bnd) atomicAdd(v + row + a, o[a]);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------- diagonal
+
+// d_l = sum_q grad phi_l(q)^T G_q grad phi_l(q), grad phi_l(q) = (DB_ia B_jb B_kc, B_ia DB_jb B_kc,
+// B_ia B_jb DB_kc): block per element, thread per node, n^3 points each (setup only).
+template <int P>
+__global__ void __launch_bounds__(256) k_diag_gauss(MeshDev m, int bc, const double* __restrict__ G, double* d) {
+  constexpr int N = P + 1, N2 = N * N, N3 = N2 * N;
+  __shared__ double sB[N2], sDB[N2];
+  for (int t = threadIdx.x; t < N2; t += blockDim.x) {
+    sB[t] = c_qB[qOffset(P) + t];
+    sDB[t] = c_qDB[qOffset(P) + t];
+  }
+  __syncthreads();
+  for (long long e = blockIdx.x; e < m.E; e += gridDim.x) {
+    int ex, ey, ez;
+    elem_coords(m, e, ex, ey, ez);
+    for (int l = threadIdx.x; l < N3; l += blockDim.x) {
+      const int a = l % N, b = (l / N) % N, c = l / N2;
+      const long long g = (long long)(ex * P + a) + (long long)m.Mx * ((long long)(ey * P + b) + (long long)m.My * (ez * P + c));
+      if (bc == 0 && lattice_boundary(m, g)) continue;
+      double s = 0.0;
+      for (int k = 0; k < N; ++k) {
+        const double Bk = sB[k * N + c], Dk = sDB[k * N + c];
+        for (int j = 0; j < N; ++j) {
+          const double Bj = sB[j * N + b], Dj = sDB[j * N + b];
+          for (int i = 0; i < N; ++i) {
+            const double Bi = sB[i * N + a], Di = sDB[i * N + a];
+            const double d0 = Di * Bj * Bk, d1 = Bi * Dj * Bk, d2 = Bi * Bj * Dk;
+            const int ij = i + N * j;
+            const double G00 = G[GLayout<P>::off(e, 0, ij, k)], G01 = G[GLayout<P>::off(e, 1, ij, k)];
+            const double G02 = G[GLayout<P>::off(e, 2, ij, k)], G11 = G[GLayout<P>::off(e, 3, ij, k)];
+            const double G12 = G[GLayout<P>::off(e, 4, ij, k)], G22 = G[GLayout<P>::off(e, 5, ij, k)];
+            s += d0 * (G00 * d0 + 2.0 * (G01 * d1 + G02 * d2)) + d1 * (G11 * d1 + 2.0 * G12 * d2) + d2 * G22 * d2;
+          }
+        }
+      }
+      atomicAdd(d + g, s);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------- load vector
+
+// Manufactured load (rhs 1): b_l = sum_q phi_l(x_q) wG_q detJ_q f(x_q), f = -div(mu grad u*) with
+// u* = sin(pi x) sin(pi y) sin(pi z); interior rows only.  Block per element: F_q in smem, then
+// the B^T x B^T x B^T contraction per node (setup only).
+template <int P>
+__global__ void __launch_bounds__(256) k_load_gauss(MeshDev m, double* f) {
+  constexpr int N = P + 1, N2 = N * N, N3 = N2 * N;
+  extern __shared__ double lsm[];
+  double* X = lsm;            // [3][N3]
+  double* F = X + 3 * N3;     // [N3]
+  double* sB = F + N3;        // [N2]
+  double* sDB = sB + N2;      // [N2]
+  const double* w = c_qw + qvOffset(P);
+  const double pi = 3.141592653589793238463;
+  for (long long e = blockIdx.x; e < m.E; e += gridDim.x) {
+    __syncthreads();
+    load_tables_and_nodes<P>(m, e, X, sB, sDB);
+    __syncthreads();
+    for (int q = threadIdx.x; q < N3; q += blockDim.x) {
+      const int i = q % N, j = (q / N) % N, k = q / N2;
+      double J[3][3], xq[3];
+      gauss_jacobian<P>(X, sB, sDB, i, j, k, J, xq);
+      const double det = J[0][0] * (J[1][1] * J[2][2] - J[1][2] * J[2][1]) -
+                         J[0][1] * (J[1][0] * J[2][2] - J[1][2] * J[2][0]) +
+                         J[0][2] * (J[1][0] * J[2][1] - J[1][1] * J[2][0]);
+      const double x = xq[0], y = xq[1], z = xq[2];
+      const double sx = sinpi(x), sy = sinpi(y), sz = sinpi(z);
+      const double us = sx * sy * sz;
+      const double gu[3] = {pi * cospi(x) * sy * sz, pi * sx * cospi(y) * sz, pi * sx * sy * cospi(z)};
+      const double mu = coeff_mu(m, x, y, z);
+      double gm[3];
+      coeff_grad(m, x, y, z, mu, gm);
+      const double fx = 3.0 * pi * pi * mu * us - (gm[0] * gu[0] + gm[1] * gu[1] + gm[2] * gu[2]);
+      F[q] = w[i] * w[j] * w[k] * det * fx;
+    }
+    __syncthreads();
+    int ex, ey, ez;
+    elem_coords(m, e, ex, ey, ez);
+    for (int l = threadIdx.x; l < N3; l += blockDim.x) {
+      const int a = l % N, b = (l / N) % N, c = l / N2;
+      const long long g = (long long)(ex * P + a) + (long long)m.Mx * ((long long)(ey * P + b) + (long long)m.My * (ez * P + c));
+      if (lattice_boundary(m, g)) continue;
+      double s = 0.0;
+      for (int k = 0; k < N; ++k)
+        for (int j = 0; j < N; ++j) {
+          const double bjk = sB[j * N + b] * sB[k * N + c];
+          for (int i = 0; i < N; ++i) s += sB[i * N + a] * bjk * F[i + N * (j + N * k)];
+        }
+      atomicAdd(f + g, s);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------- coarse CG
+
+// Single-CTA CG on a small Gauss level (the coarsest p = 1 / 2 levels of a Gauss hierarchy; R13):
+// vectors in global memory (L2-resident), thread-per-element inline apply with the Gauss tables.
+template <int P>
+__device__ void cta_apply_gauss(const MeshDev& m, const double* __restrict__ G, const double* x, double* y) {
+  constexpr int N = P + 1, N2 = N * N, N3 = N2 * N;
+  for (long long g = threadIdx.x; g < m.N; g += blockDim.x) y[g] = lattice_boundary(m, g) ? __ldcg(x + g) : 0.0;
+  __syncthreads();
+  for (long long e = threadIdx.x; e < m.E; e += blockDim.x) {
+    int ex, ey, ez;
+    elem_coords(m, e, ex, ey, ez);
+    double ue[N3], t1[N3], t2[N3];
+    long long gl[N3];
+#pragma unroll
+    for (int c = 0; c < N; ++c)
+#pragma unroll
+      for (int b = 0; b < N; ++b)
+#pragma unroll
+        for (int a = 0; a < N; ++a) {
+          const int l = a + N * (b + N * c);
+          const long long g = (long long)(ex * P + a) + (long long)m.Mx * ((long long)(ey * P + b) + (long long)m.My * (ez * P + c));
+          const bool bnd = lattice_boundary(m, g);
+          gl[l] = bnd ? -1 : g;
+          ue[l] = bnd ? 0.0 : __ldcg(x + g);
+        }
+    // u_q = (B x B x B) u_e
+#pragma unroll
+    for (int c = 0; c < N; ++c)
+#pragma unroll
+      for (int b = 0; b < N; ++b)
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          double s = 0.0;
+#pragma unroll
+          for (int a = 0; a < N; ++a) s = fma(qB<P>(i, a), ue[a + N * (b + N * c)], s);
+          t1[i + N * (b + N * c)] = s;
+        }
+#pragma unroll
+    for (int c = 0; c < N; ++c)
+#pragma unroll
+      for (int j = 0; j < N; ++j)
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          double s = 0.0;
+#pragma unroll
+          for (int b = 0; b < N; ++b) s = fma(qB<P>(j, b), t1[i + N * (b + N * c)], s);
+          t2[i + N * (j + N * c)] = s;
+        }
+#pragma unroll
+    for (int k = 0; k < N; ++k)
+#pragma unroll
+      for (int j = 0; j < N; ++j)
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          double s = 0.0;
+#pragma unroll
+          for (int c = 0; c < N; ++c) s = fma(qB<P>(k, c), t2[i + N * (j + N * c)], s);
+          ue[i + N * (j + N * k)] = s;   // u_q
+          t1[i + N * (j + N * k)] = 0.0;  // v_q accumulator
+        }
+#pragma unroll
+    for (int k = 0; k < N; ++k)
+#pragma unroll
+      for (int j = 0; j < N; ++j)
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          double g0 = 0, g1 = 0, g2 = 0;
+#pragma unroll
+          for (int mm = 0; mm < N; ++mm) {
+            g0 = fma(qDG<P>(i, mm), ue[mm + N * (j + N * k)], g0);
+            g1 = fma(qDG<P>(j, mm), ue[i + N * (mm + N * k)], g1);
+            g2 = fma(qDG<P>(k, mm), ue[i + N * (j + N * mm)], g2);
+          }
+          const int ij = i + N * j;
+          const double G00 = G[GLayout<P>::off(e, 0, ij, k)], G01 = G[GLayout<P>::off(e, 1, ij, k)];
+          const double G02 = G[GLayout<P>::off(e, 2, ij, k)], G11 = G[GLayout<P>::off(e, 3, ij, k)];
+          const double G12 = G[GLayout<P>::off(e, 4, ij, k)], G22 = G[GLayout<P>::off(e, 5, ij, k)];
+          const double w0 = G00 * g0 + G01 * g1 + G02 * g2;
+          const double w1 = G01 * g0 + G11 * g1 + G12 * g2;
+          const double w2 = G02 * g0 + G12 * g1 + G22 * g2;
+#pragma unroll
+          for (int mm = 0; mm < N; ++mm) {
+            t1[mm + N * (j + N * k)] = fma(qDG<P>(i, mm), w0, t1[mm + N * (j + N * k)]);
+            t1[i + N * (mm + N * k)] = fma(qDG<P>(j, mm), w1, t1[i + N * (mm + N * k)]);
+            t1[i + N * (j + N * mm)] = fma(qDG<P>(k, mm), w2, t1[i + N * (j + N * mm)]);
+          }
+        }
+    // v_e = (B^T x B^T x B^T) v_q
+#pragma unroll
+    for (int k = 0; k < N; ++k)
+#pragma unroll
+      for (int j = 0; j < N; ++j)
+#pragma unroll
+        for (int a = 0; a < N; ++a) {
+          double s = 0.0;
+#pragma unroll
+          for (int i = 0; i < N; ++i) s = fma(qB<P>(i, a), t1[i + N * (j + N * k)], s);
+          t2[a + N * (j + N * k)] = s;
+        }
+#pragma unroll
+    for (int k = 0; k < N; ++k)
+#pragma unroll
+      for (int b = 0; b < N; ++b)
+#pragma unroll
+        for (int a = 0; a < N; ++a) {
+          double s = 0.0;
+#pragma unroll
+          for (int j = 0; j < N; ++j) s = fma(qB<P>(j, b), t2[a + N * (j + N * k)], s);
+          t1[a + N * (b + N * k)] = s;
+        }
+#pragma unroll
+    for (int c = 0; c < N; ++c)
+#pragma unroll
+      for (int b = 0; b < N; ++b)
+#pragma unroll
+        for (int a = 0; a < N; ++a) {
+          double s = 0.0;
+#pragma unroll
+          for (int k = 0; k < N; ++k) s = fma(qB<P>(k, c), t1[a + N * (b + N * k)], s);
+          const int l = a + N * (b + N * c);
+          if (gl[l] >= 0) atomicAdd(y + gl[l], s);
+        }
+  }
+  __threadfence_block();
+  __syncthreads();
+}
+
+template <int P>
+__global__ void __launch_bounds__(256) k_coarse_cg_gauss(MeshDev m, const double* __restrict__ G, const double* b,
+                                                          double* x, double* r, double* p, double* q, double* scal,
+                                                          double rtol, int maxit) {
+  __shared__ double red[32];
+  const long long n = m.N;
+  double rr = 0.0;
+  for (long long g = threadIdx.x; g < n; g += blockDim.x) {
+    const double bg = b[g];
+    x[g] = 0.0; r[g] = bg; p[g] = bg;
+    rr += bg * bg;
+  }
+  rr = block_sum(rr, red);
+  const double bn = sqrt(rr);
+  int it = 0, status = 0;
+  if (bn > 0.0) {
+    for (; it < maxit; ++it) {
+      if (sqrt(rr) <= rtol * bn) break;
+      __syncthreads();
+      cta_apply_gauss<P>(m, G, p, q);
+      double pq = 0.0;
+      for (long long g = threadIdx.x; g < n; g += blockDim.x) pq += __ldcg(p + g) * __ldcg(q + g);
+      pq = block_sum(pq, red);
+      if (!(pq > 0.0)) { status = 6; break; }
+      const double alpha = rr / pq;
+      double rn = 0.0;
+      for (long long g = threadIdx.x; g < n; g += blockDim.x) {
+        x[g] = __ldcg(x + g) + alpha * __ldcg(p + g);
+        const double rg = __ldcg(r + g) - alpha * __ldcg(q + g);
+        r[g] = rg;
+        rn += rg * rg;
+      }
+      rn = block_sum(rn, red);
+      const double beta = rn / rr;
+      for (long long g = threadIdx.x; g < n; g += blockDim.x) p[g] = __ldcg(r + g) + beta * __ldcg(p + g);
+      rr = rn;
+      __threadfence_block();
+      __syncthreads();
+    }
+  }
+  if (threadIdx.x == 0) { scal[8] = (double)it; scal[9] = sqrt(rr); scal[10] = (double)status; }
+}
+
+// ---------------------------------------------------------------------------- launchers
+
+#define SFMG_GAUSS_DISPATCH(p, F, ...)  \
+  switch (p) {                          \
+    case 1: return F<1>(__VA_ARGS__);   \
+    case 2: return F<2>(__VA_ARGS__);   \
+    case 3: return F<3>(__VA_ARGS__);   \
+    case 4: return F<4>(__VA_ARGS__);   \
+    case 5: return F<5>(__VA_ARGS__);   \
+    case 6: return F<6>(__VA_ARGS__);   \
+    case 7: return F<7>(__VA_ARGS__);   \
+    case 8: return F<8>(__VA_ARGS__);   \
+    case 9: return F<9>(__VA_ARGS__);   \
+    case 10: return F<10>(__VA_ARGS__); \
+    case 11: return F<11>(__VA_ARGS__); \
+    case 12: return F<12>(__VA_ARGS__); \
+    case 13: return F<13>(__VA_ARGS__); \
+    case 14: return F<14>(__VA_ARGS__); \
+    case 15: return F<15>(__VA_ARGS__); \
+    case 16: return F<16>(__VA_ARGS__); \
+  }                                     \
+  return cudaErrorInvalidValue;
+
+static unsigned elem_grid(long long E) { return (unsigned)(E < 148LL * 8 ? (E > 0 ? E : 1) : 148LL * 8); }
+
+template <int P>
+static cudaError_t geometry_g(const MeshDev& m, double* G, int* bad, cudaStream_t s) {
+  constexpr int N = P + 1;
+  const size_t smem = sizeof(double) * (3 * N * N * N + 2 * N * N);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_geometry_gauss<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e) return e;
+    attr = true;
+  }
+  k_geometry_gauss<P><<<elem_grid(m.E), 256, smem, s>>>(m, G, bad);
+  return cudaGetLastError();
+}
+cudaError_t launch_geometry_gauss(const MeshDev& m, double* G, int* bad, cudaStream_t s) {
+  cudaError_t e = upload_gauss_tables(m.p);
+  if (e) return e;
+  SFMG_GAUSS_DISPATCH(m.p, geometry_g, m, G, bad, s);
+}
+
+template <int P>
+static cudaError_t apply_g(const MeshDev& m, int bc, const double* G, const double* u, double* v, cudaStream_t s) {
+  using C = GaussCfg<P>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_apply_gauss<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    if (e) return e;
+    e = cudaFuncSetAttribute(k_apply_gauss<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    if (e) return e;
+    attr = true;
+  }
+  const long long groups = (m.E + C::EPB - 1) / C::EPB;
+  const unsigned grid = (unsigned)(groups < 148LL * 16 ? groups : 148LL * 16);
+  if (bc == 0) k_apply_gauss<P, true><<<grid, C::THREADS, C::SMEM, s>>>(m, G, u, v);
+  else k_apply_gauss<P, false><<<grid, C::THREADS, C::SMEM, s>>>(m, G, u, v);
+  return cudaGetLastError();
+}
+cudaError_t launch_apply_gauss(const MeshDev& m, int bc, const double* G, const double* u, double* v, cudaStream_t s) {
+  SFMG_GAUSS_DISPATCH(m.p, apply_g, m, bc, G, u, v, s);
+}
+
+template <int P>
+static cudaError_t diag_g(const MeshDev& m, int bc, const double* G, double* d, cudaStream_t s) {
+  k_diag_gauss<P><<<elem_grid(m.E), 256, 0, s>>>(m, bc, G, d);
+  return cudaGetLastError();
+}
+cudaError_t launch_diag_gauss(const MeshDev& m, int bc, const double* G, double* d, cudaStream_t s) {
+  SFMG_GAUSS_DISPATCH(m.p, diag_g, m, bc, G, d, s);
+}
+
+template <int P>
+static cudaError_t load_g(const MeshDev& m, double* f, cudaStream_t s) {
+  constexpr int N = P + 1;
+  const size_t smem = sizeof(double) * (4 * N * N * N + 2 * N * N);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_load_gauss<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e) return e;
+    attr = true;
+  }
+  k_load_gauss<P><<<elem_grid(m.E), 256, smem, s>>>(m, f);
+  return cudaGetLastError();
+}
+cudaError_t launch_load_gauss(const MeshDev& m, double* f, cudaStream_t s) {
+  cudaError_t e = upload_gauss_tables(m.p);
+  if (e) return e;
+  SFMG_GAUSS_DISPATCH(m.p, load_g, m, f, s);
+}
+
+cudaError_t launch_coarse_cg_gauss(const MeshDev& m, const double* G, const double* b, double* x, double* r,
+                                   double* p, double* q, double* scal, double rtol, int maxit, cudaStream_t s) {
+  if (m.p == 1) k_coarse_cg_gauss<1><<<1, 256, 0, s>>>(m, G, b, x, r, p, q, scal, rtol, maxit);
+  else if (m.p == 2) k_coarse_cg_gauss<2><<<1, 256, 0, s>>>(m, G, b, x, r, p, q, scal, rtol, maxit);
+  else return cudaErrorInvalidValue;
+  return cudaGetLastError();
+}
+
+}  // namespace sfmg

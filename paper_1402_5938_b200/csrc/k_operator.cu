@@ -12,7 +12,7 @@
 // operand (no load instruction).
 #include <cstdio>
 
-#include "sfmg_internal.h"
+#include "k_common.cuh"
 
 namespace sfmg {
 
@@ -124,93 +124,6 @@ __device__ __forceinline__ void eo_line(const double (&L)[P + 1], double (&out)[
 #pragma unroll
   for (int m = 0; m < c; ++m) M = fma(c_EO[base + 2 * c * c + c + m], od[m], M);
   out[c] = M;
-}
-
-// Layout of the geometric factors, slice-major per element: G[e][k][c][j][i], c in (00,01,02,11,
-// 12,22).  An element's factors are one contiguous 48 n^3-byte block (one TMA bulk copy), and a
-// k-slice of all six components is one contiguous 48 n^2-byte block.
-template <int N>
-__device__ __forceinline__ int gofs(int c, int ij, int k) { return k * 6 * N * N + c * N * N + ij; }
-
-// Full offset of G(e, c, ij, k).  For p <= 2 (thread-per-element apply) the factors are stored
-// element-interleaved in blocks of 32 elements, [E/32][k][6][n^2][32], so that a warp in which
-// lane = element reads every component with one coalesced 256-byte access.
-template <int P>
-struct GLayout {
-  static constexpr int N = P + 1, N2 = N * N, N3 = N2 * N;
-  static constexpr bool kTPE = (P <= 2);
-  __host__ __device__ static long long padded_elems(long long E) { return kTPE ? ((E + 31) / 32) * 32 : E; }
-  __device__ static long long off(long long e, int c, int ij, int k) {
-    if (kTPE) return (((e >> 5) * 6 * N3) + (long long)(k * 6 + c) * N2 + ij) * 32 + (e & 31);
-    return e * 6 * N3 + gofs<N>(c, ij, k);
-  }
-};
-
-// element index -> (ex, ey, ez); E < 2^31 (checked at level creation), so 32-bit unsigned
-// division (a 64-bit divide costs ~5x more instructions and sits in every apply thread's loop)
-__device__ __forceinline__ void elem_coords(const MeshDev& m, long long e, int& ex, int& ey, int& ez) {
-  const unsigned ue = (unsigned)e;
-  const unsigned t = ue / (unsigned)m.nex;
-  ex = (int)(ue - t * (unsigned)m.nex);
-  ez = (int)(t / (unsigned)m.ney);
-  ey = (int)(t - (unsigned)ez * (unsigned)m.ney);
-}
-
-__device__ __forceinline__ bool lattice_boundary(const MeshDev& m, long long g) {
-  unsigned int gi = (unsigned int)g;
-  unsigned int I = gi % (unsigned)m.Mx;
-  unsigned int r = gi / (unsigned)m.Mx;
-  unsigned int J = r % (unsigned)m.My;
-  unsigned int K = r / (unsigned)m.My;
-  return I == 0 || I == (unsigned)m.Mx - 1 || J == 0 || J == (unsigned)m.My - 1 || K == 0 ||
-         K == (unsigned)m.Mz - 1;
-}
-
-// mu at a physical point (R3, R6)
-__device__ __forceinline__ double coeff_mu(const MeshDev& m, double x, double y, double z) {
-  switch (m.coeff) {
-    case 0: return m.c0;
-    case 1: return exp(m.c1 * sinpi(2.0 * x) * sinpi(2.0 * y) * sinpi(2.0 * z));
-    case 2: return exp10(m.c1 * sinpi(2.0 * x) * sinpi(2.0 * y) * sinpi(2.0 * z));
-    case 3: {
-      double a = cospi(2.0 * x), b = cospi(2.0 * y), c = cospi(2.0 * z);
-      return m.c0 + m.c1 * (a * a + b * b + c * c);
-    }
-  }
-  return 0.0;
-}
-
-__device__ __forceinline__ void coeff_grad(const MeshDev& m, double x, double y, double z, double mu,
-                                           double g[3]) {
-  const double tp = 6.283185307179586476925;
-  double sx = sinpi(2.0 * x), sy = sinpi(2.0 * y), sz = sinpi(2.0 * z);
-  double cx = cospi(2.0 * x), cy = cospi(2.0 * y), cz = cospi(2.0 * z);
-  double dS0 = tp * cx * sy * sz, dS1 = tp * sx * cy * sz, dS2 = tp * sx * sy * cz;
-  double f = 0.0;
-  switch (m.coeff) {
-    case 0: g[0] = g[1] = g[2] = 0.0; return;
-    case 1: f = m.c1 * mu; break;
-    case 2: f = 2.302585092994045684018 * m.c1 * mu; break;
-    case 3:
-      g[0] = -tp * m.c1 * sinpi(4.0 * x);
-      g[1] = -tp * m.c1 * sinpi(4.0 * y);
-      g[2] = -tp * m.c1 * sinpi(4.0 * z);
-      return;
-  }
-  g[0] = f * dS0; g[1] = f * dS1; g[2] = f * dS2;
-}
-
-// Physical position of local node (a,b,c) of element (ex,ey,ez): reference-cube lattice point
-// then the warp x_i += amp sin(pi X) sin(pi Y) sin(pi Z) (R5).
-template <int P>
-__device__ __forceinline__ void node_pos(const MeshDev& m, const double* xs, int ex, int ey, int ez,
-                                         int a, int b, int c, double X[3]) {
-  double Xr = (ex + 0.5 * (xs[a] + 1.0)) / m.nex;
-  double Yr = (ey + 0.5 * (xs[b] + 1.0)) / m.ney;
-  double Zr = (ez + 0.5 * (xs[c] + 1.0)) / m.nez;
-  double s = 0.0;
-  if (m.warp == 1) s = m.amp * sinpi(Xr) * sinpi(Yr) * sinpi(Zr);
-  X[0] = Xr + s; X[1] = Yr + s; X[2] = Zr + s;
 }
 
 // Isoparametric Jacobian at collocated point (i,j,k): J[al][be] = d x_al / d xi_be
@@ -870,17 +783,6 @@ __global__ void k_export_maps(MeshDev m, int32_t* l2g, uint8_t* mask, uint8_t* c
 // V-cycle needs no host synchronisation.  Vectors live in global memory (L2-resident at these
 // sizes) and are re-read with ld.global.cg, bypassing the incoherent L1.
 
-__device__ double block_sum(double v, double* red) {
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
-  __syncthreads();
-  if (ln == 0) red[w] = v;
-  __syncthreads();
-  double s = 0.0;
-  const int nw = (blockDim.x + 31) >> 5;
-  for (int i = 0; i < nw; ++i) s += red[i];
-  return s;
-}
 
 template <int P>
 __device__ void cta_apply(const MeshDev& m, const double* __restrict__ G, const double* x, double* y) {
@@ -1124,6 +1026,7 @@ static void geometry_p(const MeshDev& m, double* G, int* bad, cudaStream_t s) {
   k_geometry<P><<<grid_for(m.E * N3, 256), 256, 0, s>>>(m, G, bad);
 }
 cudaError_t launch_geometry(const MeshDev& m, double* G, int* bad, cudaStream_t s) {
+  if (m.quad) return launch_geometry_gauss(m, G, bad, s);
   SFMG_DISPATCH_P(m.p, geometry_p, m, G, bad, s);
   return cudaGetLastError();
 }
@@ -1190,6 +1093,7 @@ static void apply_p(const MeshDev& m, int bc, const double* G, const double* u, 
 }
 cudaError_t launch_apply(const MeshDev& m, int bc, const double* G, const double* u, double* v, int wait_mode,
                          int write_bnd, cudaStream_t s) {
+  if (m.quad) return launch_apply_gauss(m, bc, G, u, v, s);   // v initialised by the caller (no PDL)
   cudaError_t err = cudaSuccess;
   SFMG_DISPATCH_P(m.p, apply_p, m, bc, G, u, v, wait_mode, write_bnd, s, &err);
   if (err) return err;
@@ -1204,6 +1108,7 @@ static void diag_p(const MeshDev& m, int bc, const double* G, double* d, cudaStr
 cudaError_t launch_diag(const MeshDev& m, int bc, const double* G, double* d, cudaStream_t s) {
   cudaError_t e = launch_init(m, bc, nullptr, 1.0, d, s);
   if (e) return e;
+  if (m.quad) return launch_diag_gauss(m, bc, G, d, s);
   SFMG_DISPATCH_P(m.p, diag_p, m, bc, G, d, s);
   return cudaGetLastError();
 }
@@ -1217,6 +1122,7 @@ cudaError_t launch_load(const MeshDev& m, int rhs_id, double* f, cudaStream_t s)
   if (rhs_id != 1) return cudaErrorInvalidValue;
   cudaError_t e = launch_init(m, 1, nullptr, 0.0, f, s);
   if (e) return e;
+  if (m.quad) return launch_load_gauss(m, f, s);
   SFMG_DISPATCH_P(m.p, load_p, m, f, s);
   return cudaGetLastError();
 }
@@ -1255,6 +1161,7 @@ constexpr long long kCoarseSmemN = 6400;   // x, r, p, q of up to this many dofs
 
 cudaError_t launch_coarse_cg(const MeshDev& m, const double* G, const double* b, double* x, double* r,
                              double* p, double* q, double* scal, double rtol, int maxit, cudaStream_t s) {
+  if (m.quad) return launch_coarse_cg_gauss(m, G, b, x, r, p, q, scal, rtol, maxit, s);
   if (m.p != 1 && m.p != 2) return cudaErrorInvalidValue;
   if (m.N <= kCoarseSmemN) {
     const size_t smem = sizeof(double) * 4 * (size_t)m.N;

@@ -39,6 +39,7 @@ static sfmg_status check_problem(const sfmg_problem* pr) {
   if (Mx * My * Mz >= (1LL << 31)) { set_error("lattice exceeds 2^31 nodes"); return SFMG_E_MESH; }
   if (pr->warp != 0 && pr->warp != 1) { set_error("warp must be 0 or 1"); return SFMG_E_ARG; }
   if (pr->coeff < 0 || pr->coeff > 3) { set_error("coeff must be 0..3"); return SFMG_E_ARG; }
+  if (pr->quadrature != 0 && pr->quadrature != 1) { set_error("quadrature must be 0 or 1"); return SFMG_E_ARG; }
   return SFMG_OK;
 }
 
@@ -50,6 +51,7 @@ static MeshDev make_mesh(const sfmg_problem* pr) {
   m.N = (long long)m.Mx * m.My * m.Mz;
   m.warp = pr->warp; m.coeff = pr->coeff;
   m.amp = pr->warp_amp; m.c0 = pr->c0; m.c1 = pr->c1;
+  m.quad = pr->quadrature;
   return m;
 }
 
@@ -148,7 +150,7 @@ static cudaError_t element_kernel(sfmg_level_s* lv, int bc, const double* u, dou
 
 static cudaError_t op_apply(sfmg_level_s* lv, int bc, const double* u, double* v, cudaStream_t s) {
   cudaError_t e;
-  if (lv->p <= 2) {
+  if (lv->p <= 2 && !lv->m.quad) {
     e = cudaMemsetAsync(v, 0, sizeof(double) * lv->N, s);
     if (e) return e;
     return element_kernel(lv, bc, u, v, 1, 1, s);

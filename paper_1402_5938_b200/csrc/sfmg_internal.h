@@ -20,6 +20,7 @@ struct MeshDev {
   long long E, N;          // elements, dofs
   int warp, coeff;
   double amp, c0, c1;
+  int quad;                // 0 collocated LGL quadrature, 1 Gauss-Legendre (NEXT-3)
 };
 
 // Device reduction scratch: partials[kRedBlocks][kRedSlots], scalars[32], counter.
@@ -104,6 +105,16 @@ cudaError_t launch_export_maps(const MeshDev& m, int32_t* l2g, uint8_t* mask, ui
 // single-CTA CG on a (small) level: x = A_D^{-1} b to rtol (R13)
 cudaError_t launch_coarse_cg(const MeshDev& m, const double* G, const double* b, double* x, double* r,
                              double* p, double* q, double* scal, double rtol, int maxit, cudaStream_t s);
+
+// ---- Gauss-Legendre quadrature variant (k_gauss.cu, NEXT-3); the launchers above dispatch to these
+// when m.quad == 1
+cudaError_t upload_gauss_tables(int p);
+cudaError_t launch_geometry_gauss(const MeshDev& m, double* G, int* bad, cudaStream_t s);
+cudaError_t launch_apply_gauss(const MeshDev& m, int bc, const double* G, const double* u, double* v, cudaStream_t s);
+cudaError_t launch_diag_gauss(const MeshDev& m, int bc, const double* G, double* d, cudaStream_t s);
+cudaError_t launch_load_gauss(const MeshDev& m, double* f, cudaStream_t s);
+cudaError_t launch_coarse_cg_gauss(const MeshDev& m, const double* G, const double* b, double* x, double* r,
+                                   double* p, double* q, double* scal, double rtol, int maxit, cudaStream_t s);
 
 // ---- vector kernels (k_blas.cu)
 cudaError_t launch_recip(const double* d, double* dinv, long long n, cudaStream_t s);

@@ -1,0 +1,121 @@
+"""GPU <-> oracle parity of the Gauss-Legendre quadrature variant (P:430-432
+"Gauss quadrature is used to numerically approximate integrals"), through the C ABI: geometric factors
+at the Gauss points, A u (bc 0 / 1), diag, the MMS load vector, lambda_max, and the paper-settings
+hierarchy.  The oracle runs with oracle.set_quadrature(1) (pinned by test_oracle_paper_tab3dbox.py).
+Bars as in test_gpu_parity.py.
+"""
+import numpy as np
+import pytest
+
+from paper_1402_5938_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+WARP = dict(warp=1, amp=0.1, coeff=1, c0=1.0, c1=3.0)
+
+
+@pytest.fixture(scope="module")
+def S():
+    import torch
+    assert torch.cuda.is_available()
+    from paper_1402_5938_b200 import sfmg
+    return sfmg
+
+
+@pytest.fixture
+def gauss_orc(orc):
+    orc.set_quadrature(1)
+    yield orc
+    orc.set_quadrature(0)
+
+
+def to_gpu(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def levels(S, orc, d):
+    g = S.Level(S.Problem.from_dict(dict(d, quadrature=1)))
+    o = orc.Level(d["nex"], d["ney"], d["nez"], d["p"], d["warp"], d["amp"], d["coeff"], d["c0"], d["c1"])
+    return g, o
+
+
+@pytest.mark.parametrize("p,shape", [(1, (2, 3, 2)), (2, (2, 2, 3)), (3, (2, 1, 2)), (4, (2, 2, 1)), (5, (1, 2, 1)),
+                                     (8, (1, 1, 2)), (16, (1, 1, 1))])
+def test_gauss_operator_parity(S, gauss_orc, p, shape):
+    orc = gauss_orc
+    d = inputs.problem(shape[0], p, ney=shape[1], nez=shape[2], **WARP)
+    g, o = levels(S, orc, d)
+    n = p + 1
+    G = g.export_geometry().cpu().numpy().reshape(o.E, n, 6, n * n).transpose(0, 2, 1, 3).reshape(o.E, 6, n ** 3)
+    for e in range(o.E):
+        Go = o.geometry(e)[0]
+        assert np.abs(G[e] - Go).max() <= 1e-12 * np.abs(Go).max(), e
+    u = inputs.uniform_pm1(9, o.N)
+    for bc in (0, 1):
+        ref = o.apply(u, bc, tier=2)
+        got = g.apply(to_gpu(u), bc=bc).cpu().numpy()
+        assert np.abs(got - ref).max() <= 1e-11 * np.abs(ref).max(), bc
+        dref = o.diag(bc)
+        dgot = g.diag(bc).cpu().numpy()
+        assert np.abs(dgot - dref).max() <= 1e-11 * np.abs(dref).max(), bc
+    fo = o.load_vector(1)
+    fg = g.load_vector(1).cpu().numpy()
+    assert np.abs(fg - fo).max() <= 1e-11 * np.abs(fo).max()
+    if o.N > 8 and p > 1:
+        lo = o.lambda_max(10, inputs.POWER_SEED)
+        assert abs(g.lambda_max(10, inputs.POWER_SEED) - lo) <= 1e-11 * lo
+
+
+def test_gauss_affine_q1_stencil(S):
+    """Affine p = 1 with Gauss quadrature is the exact Q1 Galerkin operator: the 27-point stencil of an
+    interior node (center 8h/3, edges -h/6, corners -h/12, faces 0)."""
+    import torch
+    d = dict(inputs.problem(2, 1), quadrature=1)
+    g = S.Level(S.Problem.from_dict(d))
+    e = torch.zeros(g.N, dtype=torch.float64, device="cuda")
+    e[13] = 1.0
+    col = g.apply(e, bc=1).cpu().numpy().reshape(3, 3, 3)
+    h = 0.5
+    assert abs(col[1, 1, 1] - 8 * h / 3) < 1e-14
+    assert abs(col[1, 1, 0]) < 1e-14 and abs(col[1, 0, 0] + h / 6) < 1e-14 and abs(col[0, 0, 0] + h / 12) < 1e-14
+
+
+@pytest.mark.parametrize("smoother", ["jacobi", "cheb"])
+def test_gauss_paper_hierarchy_parity(S, gauss_orc, smoother):
+    orc = gauss_orc
+    d = dict(inputs.problem(4, 4), quadrature=1)
+    mg = S.MgParams.paper(smoother, h_levels=2)
+    H = S.Hierarchy(S.Problem.from_dict(d), mg)
+    O = orc.Hier(4, 4, 4, 4, nu_pre=mg.nu_pre, nu_post=mg.nu_post, degree=mg.cheb_degree, lo_frac=mg.eig_lo_frac,
+                 hi_frac=mg.eig_hi_frac, power_iters=mg.power_iters, seed=mg.power_seed, smoother=mg.smoother,
+                 omega=mg.jacobi_omega, lambda_method=mg.lambda_method, h_levels=2, geom_tier=2, tier=2)
+    for l in range(H.nlevels - 1):
+        assert abs(H.lam(l) - O.lam(l)) <= 1e-10 * O.lam(l), l
+    b = O.levels[0].load_vector(1)
+    for mode in (0, 1):
+        ro = O.solve(b, mode=mode, rtol=1e-8, maxit=200)
+        _, rg = H.solve(to_gpu(b), mode=mode, rtol=1e-8, max_iter=200)
+        assert rg["converged"] and ro["converged"]
+        assert abs(rg["iterations"] - ro["iterations"]) <= 1, (mode, rg["iterations"], ro["iterations"])
+
+
+def test_gauss_tab_3d_box_on_gpu(S):
+    """tab:3d-box (tests/golden/tab_3d_box.txt): the GPU with Gauss quadrature and the
+    paper's settings reproduces the printed p-multigrid iteration counts to +-1 for p = 1, 2, 4."""
+    import os
+    rows = {}
+    for line in open(os.path.join(os.path.dirname(__file__), "golden", "tab_3d_box.txt")):
+        if line.strip() and not line.startswith("#"):
+            v = [int(t) for t in line.split()]
+            rows[v[0]] = v[1:]
+    for p in (1, 2, 4):
+        d = dict(inputs.problem(8, p), quadrature=1)
+        ours = []
+        for mode in (0, 1):
+            for sm in ("jacobi", "cheb"):
+                H = S.Hierarchy(S.Problem.from_dict(d), S.MgParams.paper(sm, h_levels=2))
+                b = H.levels[0].load_vector(1)
+                _, rep = H.solve(b, mode=mode, rtol=1e-8, max_iter=200)
+                assert rep["converged"]
+                ours.append(rep["iterations"])
+        assert np.all(np.abs(np.array(ours) - np.array(rows[p])) <= 1), (p, ours, rows[p])
