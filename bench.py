@@ -434,6 +434,19 @@ def run_extras(args, sfmg, dev, stream, flush, hbm_peak):
                                             "solve_ms": a.elapsed_time(e), "fine_applies": rep["fine_applies"]}
         del H
     out["next1_3dconst_p16_paper_settings"] = nx
+    # NEXT-3: Gauss-Legendre quadrature variant of the apply (config-3 meshes)
+    gq = []
+    for p in (4, 8, 16):
+        d = dict(inputs.CONFIG3[p], quadrature=1)
+        alg = algorithmic(d)
+        lv = sfmg.Level(sfmg.Problem.from_dict(d), device=dev)
+        u = torch.from_numpy(inputs.uniform_pm1(inputs.SEEDS[3], lv.N)).to(dev)
+        v = torch.empty_like(u)
+        ta = time_events(lambda: lv.apply(u, v), stream, flush, 10)
+        gq.append({"p": p, "apply_us": ta * 1e6, "apply_gdofs": lv.N / ta / 1e9,
+                   "apply_hbm_frac": alg["apply_bytes"] / ta / 1e9 / hbm_peak})
+        del lv, u, v
+    out["next3_gauss_apply_config3"] = gq
     return out
 
 
