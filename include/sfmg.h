@@ -167,6 +167,13 @@ sfmg_status sfmg_load_vector(sfmg_level lv, int32_t rhs_id, double* d_f, int64_t
  * device scratch, run the call, copy the result back; syncs.  h_* have length N. */
 sfmg_status sfmg_apply_host(sfmg_level lv, int32_t bc, const double* h_u, double* h_v, int64_t n,
                             void* stream);
+/* sfmg_apply_host is pipelined over z-slabs of element layers: the host->device copy of slab c+1,
+ * the kernels of slab c and the device->host copy of slab c-1 run concurrently (two internal copy
+ * streams ordered after the caller's prior work on `stream`; the call syncs).  The result is the
+ * same A_D u up to the summation order of the scatter.  slabs = 0 (default): automatic (<= 8
+ * slabs of >= ~1 MB, 1 for Gauss quadrature); k > 0: min(k, 8, nez) slabs.  p <= 2 needs
+ * nex*ney % 32 == 0 to split (else 1 slab). */
+sfmg_status sfmg_host_pipeline(sfmg_level lv, int32_t slabs);
 sfmg_status sfmg_cheb_host(sfmg_level lv, const double* h_b, double* h_x, int64_t n,
                            int32_t degree, double lam_lo, double lam_hi, void* stream);
 

@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
 #pragma unroll
     for (int k = 0; k < N; ++k) {
       bool ok = act;
-      if (DIR) { const int K = ez * P + k; ok = ok && !(bxy || K == 0 || K == m.Mz - 1); }
+      if (DIR) { const int K = ez * P + k; ok = ok && !(bxy || K == m.Kb0 || K == m.Kb1); }
       r[k] = ok ? __ldg(u + col + sxy * k) : 0.0;
     }
   };
@@ -536,7 +536,7 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
 #pragma unroll
       for (int c = 0; c < N; ++c) {
         bool bnd = false;
-        if (DIR) { const int K = ez * P + c; bnd = bxy || K == 0 || K == m.Mz - 1; }
+        if (DIR) { const int K = ez * P + c; bnd = bxy || K == m.Kb0 || K == m.Kb1; }
         if (!bnd) atomicAdd(v + gcol + sxy * c, su[t + N2 * c] + vz[c]);
         else if (write_bnd && own_xy && (c > 0 || ez == 0)) v[gcol + sxy * c] = u[gcol + sxy * c];  // (I-M) u
       }
@@ -575,7 +575,7 @@ __global__ void __launch_bounds__(128) k_apply_tpe(MeshDev m, const double* __re
           bool bnd = false;
           if (DIR) {
             const int I = ex * P + a, J = ey * P + b, K = ez * P + c;
-            bnd = I == 0 || I == m.Mx - 1 || J == 0 || J == m.My - 1 || K == 0 || K == m.Mz - 1;
+            bnd = I == 0 || I == m.Mx - 1 || J == 0 || J == m.My - 1 || K == m.Kb0 || K == m.Kb1;
           }
           ue[l] = bnd ? 0.0 : __ldg(u + g0 + a + (long long)m.Mx * b + sxy * c);
           ve[l] = 0.0;
@@ -620,7 +620,7 @@ __global__ void __launch_bounds__(128) k_apply_tpe(MeshDev m, const double* __re
           bool bnd = false;
           if (DIR) {
             const int I = ex * P + a, J = ey * P + b, K = ez * P + c;
-            bnd = I == 0 || I == m.Mx - 1 || J == 0 || J == m.My - 1 || K == 0 || K == m.Mz - 1;
+            bnd = I == 0 || I == m.Mx - 1 || J == 0 || J == m.My - 1 || K == m.Kb0 || K == m.Kb1;
           }
           const long long g = g0 + a + (long long)m.Mx * b + sxy * c;
           if (!bnd) atomicAdd(v + g, ve[a + N * (b + N * c)]);
@@ -729,7 +729,7 @@ __global__ void __launch_bounds__(256) k_init(MeshDev m, int bc, const double* _
   for (long long r = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += wstride) {
     const unsigned r32 = (unsigned)r;
     const int K = (int)(r32 / (unsigned)m.My), J = (int)(r32 - (unsigned)K * (unsigned)m.My);
-    const bool rowb = (bc == 0) && (J == 0 || J == m.My - 1 || K == 0 || K == m.Mz - 1);
+    const bool rowb = (bc == 0) && (J == 0 || J == m.My - 1 || K == m.Kb0 || K == m.Kb1);
     double* vr = v + r * m.Mx;
     const double* ur = u ? u + r * m.Mx : nullptr;
     for (int I = lane; I < m.Mx; I += 32) {

@@ -52,6 +52,7 @@ static MeshDev make_mesh(const sfmg_problem* pr) {
   m.warp = pr->warp; m.coeff = pr->coeff;
   m.amp = pr->warp_amp; m.c0 = pr->c0; m.c1 = pr->c1;
   m.quad = pr->quadrature;
+  m.Kb0 = 0; m.Kb1 = m.Mz - 1;
   return m;
 }
 
@@ -312,6 +313,11 @@ static void free_prof(sfmg_level_s* lv) {
   for (cudaEvent_t ev : lv->prof_ev) cudaEventDestroy(ev);
   lv->prof_ev.clear();
   lv->prof_used = 0;
+  for (cudaEvent_t ev : lv->hp_ev) cudaEventDestroy(ev);
+  lv->hp_ev.clear();
+  if (lv->hp_h2d) cudaStreamDestroy(lv->hp_h2d);
+  if (lv->hp_d2h) cudaStreamDestroy(lv->hp_d2h);
+  lv->hp_h2d = lv->hp_d2h = nullptr;
 }
 
 sfmg_status sfmg_level_destroy(sfmg_level lv) {
@@ -443,15 +449,109 @@ sfmg_status sfmg_load_vector(sfmg_level lv, int32_t rhs_id, double* d_f, int64_t
   return SFMG_OK;
 }
 
+// Host-buffer apply, pipelined over z-slabs of element layers: the H2D copy of slab c+1, the
+// kernels of slab c and the D2H copy of slab c-1 overlap (copy engines in both directions + SMs).
+// Slab c = element layers [L_c, L_{c+1}) reads u planes [L_c p, L_{c+1} p] and adds into the same
+// v planes; its kernels run on a z-slab view of the lattice whose cut planes are not Dirichlet
+// planes (MeshDev::Kb0/Kb1).  v plane L_{c+1} p also receives slab c+1, so slab c ships v planes
+// [L_c p, L_{c+1} p) after its kernels and the last slab the rest.  Same arithmetic as sfmg_apply.
+static constexpr int kHostChunks = 8;
+
+static int host_chunks(const sfmg_level_s* lv) {
+  if (lv->m.quad) return 1;
+  if (lv->p <= 2 && ((long long)lv->m.nex * lv->m.ney) % 32 != 0) return 1;   // interleaved G blocks of 32
+  if (lv->hp_slabs > 0) return std::min(std::min(lv->hp_slabs, kHostChunks), lv->m.nez);
+  const long long plane_bytes = (long long)lv->m.Mx * lv->m.My * 8;
+  long long S = std::min<long long>(lv->m.nez, kHostChunks);
+  S = std::min<long long>(S, std::max<long long>(1, plane_bytes * lv->m.Mz / (1 << 20)));   // >= ~1 MB per slab
+  return (int)std::max<long long>(S, 1);
+}
+
+static cudaError_t host_pipe_ready(sfmg_level_s* lv) {
+  cudaError_t e;
+  if (!lv->hp_h2d && (e = cudaStreamCreateWithFlags(&lv->hp_h2d, cudaStreamNonBlocking))) return e;
+  if (!lv->hp_d2h && (e = cudaStreamCreateWithFlags(&lv->hp_d2h, cudaStreamNonBlocking))) return e;
+  while (lv->hp_ev.size() < 1 + 3 * (size_t)kHostChunks) {
+    cudaEvent_t ev;
+    if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming))) return e;
+    lv->hp_ev.push_back(ev);
+  }
+  return cudaSuccess;
+}
+
+// z-slab view of planes [K0, K0 + planes) (Kb0/Kb1 keep only the true boundary planes)
+static MeshDev slab_view(const MeshDev& m, int K0, int planes, int nez) {
+  MeshDev v = m;
+  v.nez = nez;
+  v.Mz = planes;
+  v.E = (long long)m.nex * m.ney * nez;
+  v.N = (long long)m.Mx * m.My * planes;
+  v.Kb0 = (K0 == 0) ? 0 : -1;
+  v.Kb1 = (K0 + planes == m.Mz) ? planes - 1 : -1;
+  return v;
+}
+
 sfmg_status sfmg_apply_host(sfmg_level lv, int32_t bc, const double* h_u, double* h_v, int64_t n, void* stream) {
   if (!lv || !h_u || !h_v || (bc != 0 && bc != 1)) return SFMG_E_ARG;
   if (n != lv->N) return SFMG_E_ARG;
   cudaStream_t s = (cudaStream_t)stream;
   const size_t bytes = sizeof(double) * lv->N;
-  CK(cudaMemcpyAsync(lv->t1, h_u, bytes, cudaMemcpyHostToDevice, s));
-  CK(op_apply(lv, bc, lv->t1, lv->t2, s));
-  CK(cudaMemcpyAsync(h_v, lv->t2, bytes, cudaMemcpyDeviceToHost, s));
+  const int S = host_chunks(lv);
+  if (S <= 1) {
+    CK(cudaMemcpyAsync(lv->t1, h_u, bytes, cudaMemcpyHostToDevice, s));
+    CK(op_apply(lv, bc, lv->t1, lv->t2, s));
+    CK(cudaMemcpyAsync(h_v, lv->t2, bytes, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return SFMG_OK;
+  }
+  CK(host_pipe_ready(lv));
+  const MeshDev& m = lv->m;
+  const int p = lv->p;
+  const long long sxy = (long long)m.Mx * m.My;
+  const long long n3 = lv->n3;
+  int L[kHostChunks + 1];
+  for (int c = 0; c <= S; ++c) L[c] = (int)((long long)m.nez * c / S);
+  cudaEvent_t* ev = lv->hp_ev.data();
+  CK(cudaEventRecord(ev[0], s));   // the copies start after the caller's prior work on s
+  CK(cudaStreamWaitEvent(lv->hp_h2d, ev[0], 0));
+  CK(cudaStreamWaitEvent(lv->hp_d2h, ev[0], 0));
+  for (int c = 0; c < S; ++c) {   // H2D: u planes not yet on the device
+    const long long k0 = (c == 0) ? 0 : (long long)L[c] * p + 1, k1 = (long long)L[c + 1] * p;
+    CK(cudaMemcpyAsync(lv->t1 + k0 * sxy, h_u + k0 * sxy, sizeof(double) * (k1 - k0 + 1) * sxy,
+                       cudaMemcpyHostToDevice, lv->hp_h2d));
+    CK(cudaEventRecord(ev[1 + 3 * c], lv->hp_h2d));
+  }
+  for (int c = 0; c < S; ++c) {   // kernels of slab c on the caller's stream
+    CK(cudaStreamWaitEvent(s, ev[1 + 3 * c], 0));
+    const int K0 = L[c] * p, K1 = L[c + 1] * p;
+    const int i0 = (c == 0) ? 0 : K0 + 1;   // plane K0 was initialised (and partly summed) by slab c-1
+    const MeshDev mi = slab_view(m, i0, K1 - i0 + 1, L[c + 1] - L[c]);
+    const MeshDev ma = slab_view(m, K0, K1 - K0 + 1, L[c + 1] - L[c]);
+    const double* Ga = lv->G + (long long)L[c] * m.nex * m.ney * 6 * n3;
+    if (p <= 2) {
+      CK(cudaMemsetAsync(lv->t2 + i0 * sxy, 0, sizeof(double) * (K1 - i0 + 1) * sxy, s));
+      CK(launch_apply(ma, bc, Ga, lv->t1 + K0 * sxy, lv->t2 + K0 * sxy, 1, 1, s));
+    } else {
+      CK(launch_init(mi, bc, lv->t1 + i0 * sxy, 0.0, lv->t2 + i0 * sxy, s));
+      CK(launch_apply(ma, bc, Ga, lv->t1 + K0 * sxy, lv->t2 + K0 * sxy, 1, 0, s));
+    }
+    CK(cudaEventRecord(ev[2 + 3 * c], s));
+  }
+  for (int c = 0; c < S; ++c) {   // D2H: v planes complete after slab c
+    const long long k0 = (c == 0) ? 0 : (long long)L[c] * p, k1 = (c == S - 1) ? m.Mz : (long long)L[c + 1] * p;
+    CK(cudaStreamWaitEvent(lv->hp_d2h, ev[2 + 3 * c], 0));
+    CK(cudaMemcpyAsync(h_v + k0 * sxy, lv->t2 + k0 * sxy, sizeof(double) * (k1 - k0) * sxy, cudaMemcpyDeviceToHost,
+                       lv->hp_d2h));
+    CK(cudaEventRecord(ev[3 + 3 * c], lv->hp_d2h));
+  }
+  CK(cudaStreamWaitEvent(s, ev[3 + 3 * (S - 1)], 0));
   CK(cudaStreamSynchronize(s));
+  return SFMG_OK;
+}
+
+sfmg_status sfmg_host_pipeline(sfmg_level lv, int32_t slabs) {
+  if (!lv || slabs < 0) return SFMG_E_ARG;
+  lv->hp_slabs = slabs;
   return SFMG_OK;
 }
 

@@ -21,6 +21,10 @@ struct MeshDev {
   int warp, coeff;
   double amp, c0, c1;
   int quad;                // 0 collocated LGL quadrature, 1 Gauss-Legendre (NEXT-3)
+  // lattice planes K that lie on the Dirichlet boundary z = 0 / z = 1: 0 and Mz - 1 for a whole
+  // mesh; a z-slab view (pipelined host apply) marks an interior cut plane with -1.  Used by the
+  // apply and init kernels only.
+  int Kb0, Kb1;
 };
 
 // Device reduction scratch: partials[kRedBlocks][kRedSlots], scalars[32], counter.
@@ -61,6 +65,10 @@ struct sfmg_level_s {
   bool prof = false;
   std::vector<cudaEvent_t> prof_ev;   // [2 * launches]
   size_t prof_used = 0;
+  // pipelined host-buffer apply (sfmg_apply_host): copy streams and per-chunk events, made lazily
+  cudaStream_t hp_h2d = nullptr, hp_d2h = nullptr;
+  int hp_slabs = 0;                 // 0: automatic slab count, else forced (sfmg_host_pipeline)
+  std::vector<cudaEvent_t> hp_ev;   // [0] start, then [1 + 3c + {0,1,2}] = H2D / compute / D2H done
 };
 
 struct sfmg_hier_s {

@@ -76,6 +76,7 @@ _SIG = {
     "sfmg_load_vector": ([_vp, _i32, _vp, _i64, _vp], C.c_int),
     "sfmg_apply_host": ([_vp, _i32, _vp, _vp, _i64, _vp], C.c_int),
     "sfmg_cheb_host": ([_vp, _vp, _vp, _i64, _i32, _d, _d, _vp], C.c_int),
+    "sfmg_host_pipeline": ([_vp, _i32], C.c_int),
     "sfmg_profile_enable": ([_vp, _i32], C.c_int),
     "sfmg_profile_read": ([_vp, _P(_d), _P(_i64), _i32], C.c_int),
     "sfmg_prolong": ([_vp, _vp, _vp, _vp, _vp], C.c_int),
@@ -273,6 +274,10 @@ class Level:
         _ck(_lib.sfmg_apply_host(self.h, bc, u.ctypes.data_as(_vp), v.ctypes.data_as(_vp), self.N,
                                  _stream(stream)), "sfmg_apply_host")
         return v
+
+    def host_pipeline(self, slabs: int = 0):
+        """Slab count of the pipelined apply_host (0 = automatic)."""
+        _ck(_lib.sfmg_host_pipeline(self.h, slabs), "sfmg_host_pipeline")
 
     def cheb_host(self, b: np.ndarray, x: np.ndarray, degree, lam_lo, lam_hi, stream=None):
         """In place on the host array x."""

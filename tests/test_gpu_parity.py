@@ -256,3 +256,27 @@ def test_zero_rhs_solve(S):
         x, rep = H.solve(b, mode=mode)
         assert rep["converged"] and rep["iterations"] == 0
         assert float(x.abs().max()) == 0.0
+
+
+PIPE = [inputs.problem(4, 1, ney=8, nez=5, **WARP), inputs.problem(8, 2, ney=4, nez=3, **WARP),
+        inputs.problem(3, 3, ney=2, nez=7, **WARP), inputs.problem(2, 8, ney=3, nez=4, **WARP),
+        inputs.problem(2, 4, ney=2, nez=3, warp=0, coeff=0), inputs.problem(1, 16, ney=1, nez=2, **WARP)]
+
+
+@pytest.mark.parametrize("d", PIPE, ids=_id)
+@pytest.mark.parametrize("bc", [0, 1])
+def test_apply_host_pipelined_slabs(S, orc, d, bc):
+    """sfmg_apply_host split into z-slabs (host_pipeline): every slab count gives the oracle's A u
+    (the cut planes are summed by two slabs, the true boundary planes pass u through)."""
+    g = gpu_level(S, d)
+    o = orc_level(orc, d)
+    u = inputs.uniform_pm1(7, o.N)
+    ref = o.apply(u, bc, tier=2)
+    scale = np.abs(ref).max()
+    dev = g.apply(to_gpu(u), bc=bc).cpu().numpy()
+    for slabs in (1, 2, 3, d["nez"], 8):
+        g.host_pipeline(slabs)
+        got = g.apply_host(u, bc=bc)
+        assert rel_err(got, ref, scale) <= 1e-11, slabs
+        np.testing.assert_allclose(got, dev, rtol=0, atol=1e-14 * scale)
+    g.host_pipeline(0)
