@@ -82,6 +82,9 @@ def lib():
         L.orc_hier_create2.restype = vp
         L.orc_hier_create2.argtypes = [i, i, i, i, i, d, i, d, d, i, i, i, d, d, i, u64, d, i, i, i,
                                        i, d, i, i, C.POINTER(C.c_int)]
+        L.orc_hier_create3.restype = vp
+        L.orc_hier_create3.argtypes = [i, i, i, i, i, d, i, d, d, i, i, i, d, d, i, u64, d, i, i, i,
+                                       i, d, i, i, i, C.POINTER(C.c_int)]
         L.orc_prolong.argtypes = [vp, vp, vp, vp]
         L.orc_restrict.argtypes = [vp, vp, vp, vp]
         L.orc_load_vector.argtypes = [vp, i, vp]
@@ -338,19 +341,20 @@ class _LevelView(Level):
 
 
 class Hier:
-    """p-multigrid hierarchy p, p/2, ..., 1 (+ h_levels geometric coarsenings of the p = 1 mesh).
+    """p-multigrid hierarchy p, p/2, ..., 1 (+ h_levels geometric coarsenings of the p = 1 mesh);
+    coarsen=1: high-order h-multigrid, order p on meshes ne, ne/2, ..., ne/2^h_levels (NEXT-4).
     smoother 0: Chebyshev-Jacobi of `degree`; 1: damped point Jacobi (omega), one step per smoothing
     application.  lambda_method 0: power iteration (R9); 1: Arnoldi (R26)."""
 
     def __init__(self, nex, ney, nez, p, warp=0, amp=0.0, coeff=0, c0=1.0, c1=0.0,
                  nu_pre=2, nu_post=2, degree=4, lo_frac=0.1, hi_frac=1.1, power_iters=10,
                  seed=12345, coarse_rtol=1e-10, coarse_maxit=10000, geom_tier=3, tier=3,
-                 smoother=0, omega=2.0 / 3.0, lambda_method=0, h_levels=0):
+                 smoother=0, omega=2.0 / 3.0, lambda_method=0, h_levels=0, coarsen=0):
         st = C.c_int(0)
-        self.h = lib().orc_hier_create2(nex, ney, nez, p, warp, amp, coeff, c0, c1, nu_pre, nu_post,
+        self.h = lib().orc_hier_create3(nex, ney, nez, p, warp, amp, coeff, c0, c1, nu_pre, nu_post,
                                         degree, lo_frac, hi_frac, power_iters, seed, coarse_rtol,
                                         coarse_maxit, geom_tier, tier, smoother, omega, lambda_method,
-                                        h_levels, C.byref(st))
+                                        h_levels, coarsen, C.byref(st))
         self.status = st.value
         if not self.h:
             raise ValueError("cannot build hierarchy (status %d)" % st.value)
@@ -360,10 +364,10 @@ class Hier:
         q = p
         while True:
             orders.append(q)
-            if q == 1:
+            if q == 1 or coarsen == 1:
                 break
             q //= 2
-        orders += [1] * h_levels
+        orders += [orders[-1]] * h_levels
         for lv, q in zip(self.levels, orders):
             lv.p = q
             lv.n = q + 1

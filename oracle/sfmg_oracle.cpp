@@ -1304,17 +1304,20 @@ int orc_cg_dense(int n, const double* A, const double* b, double* x, double rtol
   return 0;
 }
 
-// p-multigrid hierarchy p, p/2, ..., 1 on one element grid (R20), followed by h_levels
-// geometric coarsenings of the p = 1 mesh (ne -> ne/2 -> ...; NEXT-1).
+// coarsen 0: p-multigrid hierarchy p, p/2, ..., 1 on one element grid (R20), followed by
+// h_levels geometric coarsenings of the p = 1 mesh (ne -> ne/2 -> ...; NEXT-1).
+// coarsen 1: high-order h-multigrid (NEXT-4): order p on meshes ne, ne/2, ..., ne/2^h_levels
+// ("three levels with 8x8x8, 4x4x4 and 2x2x2 elements"), any p.
 // smoother 0: Chebyshev-Jacobi of degree K; 1: damped point Jacobi (omega), one step per smoothing
 // application.  lambda_method 0: power iteration (R9), 1: Arnoldi (R26), power_iters steps.
-void* orc_hier_create2(int nex, int ney, int nez, int p, int warp, double amp, int coeff, double c0,
+void* orc_hier_create3(int nex, int ney, int nez, int p, int warp, double amp, int coeff, double c0,
                        double c1, int nu_pre, int nu_post, int K, double lo_frac, double hi_frac,
                        int power_iters, uint64_t seed, double coarse_rtol, int coarse_maxit,
                        int geom_tier, int tier, int smoother, double omega, int lambda_method, int h_levels,
-                       int* status) {
+                       int coarsen, int* status) {
   *status = 0;
-  for (int q = p; q > 1; q /= 2)
+  const int p_levels_to = (coarsen == 1) ? p : 1;   // orders kept: p, ..., p_levels_to
+  for (int q = p; q > p_levels_to; q /= 2)
     if (q % 2) { *status = 5; return nullptr; }
   for (int j = 0; j < h_levels; ++j)
     if (((nex >> j) % 2) || ((ney >> j) % 2) || ((nez >> j) % 2)) { *status = 5; return nullptr; }
@@ -1322,15 +1325,16 @@ void* orc_hier_create2(int nex, int ney, int nez, int p, int warp, double amp, i
   H->nu_pre = nu_pre; H->nu_post = nu_post; H->K = K; H->lo_frac = lo_frac; H->hi_frac = hi_frac;
   H->power_iters = power_iters; H->seed = seed; H->coarse_rtol = coarse_rtol; H->coarse_maxit = coarse_maxit;
   H->smoother = smoother; H->omega = omega; H->lambda_method = lambda_method;
-  for (int q = p; q >= 1; q /= 2) {
+  for (int q = p; q >= p_levels_to; q /= 2) {
     Level* L = (Level*)orc_level_create(nex, ney, nez, q, warp, amp, coeff, c0, c1, 1, geom_tier, tier);
     if (!L) { *status = 1; return H; }
     if (L->status) *status = L->status;
     H->lv.push_back(L);
-    if (q == 1) break;
+    if (q == p_levels_to) break;
   }
   for (int j = 1; j <= h_levels; ++j) {
-    Level* L = (Level*)orc_level_create(nex >> j, ney >> j, nez >> j, 1, warp, amp, coeff, c0, c1, 1, geom_tier, tier);
+    Level* L = (Level*)orc_level_create(nex >> j, ney >> j, nez >> j, p_levels_to, warp, amp, coeff, c0, c1, 1,
+                                        geom_tier, tier);
     if (!L) { *status = 1; return H; }
     if (L->status) *status = L->status;
     H->lv.push_back(L);
@@ -1340,6 +1344,16 @@ void* orc_hier_create2(int nex, int ney, int nez, int p, int warp, double amp, i
     H->lam[l] = lambda_method == 1 ? lambda_arnoldi(*H->lv[l], power_iters, seed, nullptr)
                                    : lambda_max(*H->lv[l], power_iters, seed, nullptr);
   return H;
+}
+
+void* orc_hier_create2(int nex, int ney, int nez, int p, int warp, double amp, int coeff, double c0,
+                       double c1, int nu_pre, int nu_post, int K, double lo_frac, double hi_frac,
+                       int power_iters, uint64_t seed, double coarse_rtol, int coarse_maxit,
+                       int geom_tier, int tier, int smoother, double omega, int lambda_method, int h_levels,
+                       int* status) {
+  return orc_hier_create3(nex, ney, nez, p, warp, amp, coeff, c0, c1, nu_pre, nu_post, K, lo_frac, hi_frac,
+                          power_iters, seed, coarse_rtol, coarse_maxit, geom_tier, tier, smoother, omega,
+                          lambda_method, h_levels, 0, status);
 }
 
 void* orc_hier_create(int nex, int ney, int nez, int p, int warp, double amp, int coeff, double c0,

@@ -40,7 +40,8 @@ def np_P0_h(shape_c, p, mask_c, mask_f, hat=False):
     return np.diag(1.0 - mask_f) @ P @ np.diag(1.0 - mask_c)
 
 
-@pytest.mark.parametrize("shape_c,p", [((1, 1, 1), 1), ((2, 2, 2), 1), ((2, 1, 3), 1), ((1, 2, 1), 2)])
+@pytest.mark.parametrize("shape_c,p", [((1, 1, 1), 1), ((2, 2, 2), 1), ((2, 1, 3), 1), ((1, 2, 1), 2),
+                                       ((1, 1, 2), 3), ((1, 1, 1), 4)])
 def test_h_prolong_restrict_against_hats_and_adjoint(orc, shape_c, p):
     C = orc.Level(*shape_c, p, **WARPED)
     F = orc.Level(*[2 * s for s in shape_c], p, **WARPED)
@@ -140,6 +141,58 @@ def test_paper_hierarchy_counters(orc):
     H = orc.Hier(4, 4, 4, 4, nu_pre=3, nu_post=3, smoother=1, lambda_method=1, h_levels=2, **WARPED)
     assert H.nlevels == 5
     assert [lv.N for lv in H.levels] == [17 ** 3, 9 ** 3, 5 ** 3, 3 ** 3, 2 ** 3]
+    b = H.levels[0].load_vector(1)
+    mg = H.solve(b, mode=0, rtol=1e-8)
+    pcg = H.solve(b, mode=1, rtol=1e-8)
+    assert mg["converged"] and pcg["converged"]
+    assert mg["fine_applies"] == mg["iterations"] * (7 + 1)
+    assert pcg["fine_applies"] == pcg["iterations"] * (7 + 1)
+    assert pcg["iterations"] <= mg["iterations"]
+    r = b - H.levels[0].apply(pcg["x"], 0, tier=3)
+    assert np.linalg.norm(r) <= 1.0000001e-8 * np.linalg.norm(b)
+
+
+# ------------------------------------------------------------------ NEXT-4: high-order h-multigrid
+
+
+def test_vcycle_two_level_high_order_h_pair(orc):
+    """NEXT-4: two-level V(2,2) with degree-3 Chebyshev smoothing at order p = 2 on meshes
+    2x2x2 -> 1x1x1 (coarsen = 1 keeps the order) equals the closed form (I - S C S) A^{-1} with
+    S = T_3((theta - D^-1 A)/delta) / T_3(theta/delta) squared and C = I - P0 A_c^{-1} P0^T A, P0 from
+    the independent global 1-D Lagrange construction."""
+    kw = dict(nu_pre=2, nu_post=2, degree=3, coarse_rtol=1e-15, geom_tier=2, tier=2, h_levels=1, coarsen=1)
+    H = orc.Hier(2, 2, 2, 2, **WARPED, **kw)
+    assert H.nlevels == 2 and [lv.N for lv in H.levels] == [125, 27]
+    F, Cl = H.levels
+    A = F.assemble_dense(0)
+    Ac = Cl.assemble_dense(0)
+    P0 = np_P0_h((1, 1, 1), 2, Cl.mask().astype(float), F.mask().astype(float))
+    d = np.diag(A)
+    lam = H.lam(0)
+    lo, hi = 0.1 * lam, 1.1 * lam
+    theta, delta = 0.5 * (hi + lo), 0.5 * (hi - lo)
+    X = (theta * np.eye(F.N) - A / d[:, None]) / delta
+    T = [np.eye(F.N), X]
+    for _ in range(2):
+        T.append(2 * X @ T[-1] - T[-2])
+    s3 = np.cosh(3 * np.arccosh(theta / delta))
+    E = T[3] / s3   # degree-3 Chebyshev error propagator (R7)
+    S = E @ E
+    Cc = np.eye(F.N) - P0 @ np.linalg.solve(Ac, P0.T @ A)
+    Bref = (np.eye(F.N) - S @ Cc @ S) @ np.linalg.inv(A)
+    B = np.stack([H.vcycle(np.eye(F.N)[i]) for i in range(F.N)], axis=1)
+    sc = np.abs(Bref).max()
+    np.testing.assert_allclose(B, Bref, rtol=0, atol=1e-9 * sc)
+
+
+@pytest.mark.parametrize("p", [1, 3])
+def test_high_order_h_hierarchy_counters(orc, p):
+    """three meshes at one order (odd p allowed, no p-coarsening); Cheb(3,3) costs one
+    residual and six fine applies per V-cycle; pCG <= MG-solver iterations."""
+    H = orc.Hier(4, 4, 4, p, nu_pre=1, nu_post=1, degree=3, lo_frac=0.25, hi_frac=1.0, lambda_method=1,
+                 h_levels=2, coarsen=1, **WARPED)
+    assert H.nlevels == 3
+    assert [lv.N for lv in H.levels] == [(4 * p + 1) ** 3, (2 * p + 1) ** 3, (p + 1) ** 3]
     b = H.levels[0].load_vector(1)
     mg = H.solve(b, mode=0, rtol=1e-8)
     pcg = H.solve(b, mode=1, rtol=1e-8)
