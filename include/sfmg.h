@@ -85,6 +85,12 @@ typedef struct {
   int32_t h_levels;          /* geometric coarsenings of the p = 1 mesh after p-coarsening     */
                              /*    (ne -> ne/2, trilinear h-transfer); */
                              /*    every ne must be divisible by 2^h_levels                   */
+  int32_t coarsen;           /* 0: p-multigrid p, p/2, ..., 1, then h_levels at p = 1 (above); */
+                             /* 1: high-order h-multigrid:    */
+                             /*    order p (any 1..16) on meshes ne, ne/2, ..., ne/2^h_levels  */
+                             /*    (h_levels >= 1), transfer = eq. (7) between nested meshes. */
+                             /*    A coarsest order > 2 is solved by a host-polled CG, so that */
+                             /*    V-cycle is not replayed as a CUDA graph                    */
 } sfmg_mg_params;
 
 /* Solve report.  history: caller-owned host buffer of history_cap doubles
@@ -187,8 +193,9 @@ sfmg_status sfmg_profile_read(sfmg_level lv, double* ms, int64_t* launches, int3
 
 /* ---------------------------------------------------------------- transfer */
 /* p pair: fine.order == 2 coarse.order on the same element grid (coarse.order <= 8); or h pair:
- * both order 1, fine.ne == 2 coarse.ne in every direction (nesting in reference-
- * lattice coordinates, R25).  Anything else: SFMG_E_PCOARSEN.
+ * one order (1..16), fine.ne == 2 coarse.ne in every direction (nesting in
+ * reference-lattice coordinates, R25; fine element e is child (ex&1, ey&1, ez&1) of coarse element
+ * (ex/2, ey/2, ez/2)).  Anything else: SFMG_E_PCOARSEN.
  * prolong: d_uf = P0 d_uc with P0 = M_f P M_c, P_gJ = phi^{coarse}_J(xi(g)) (eq. (7)).
  * restrict: d_rc = P0^T d_rf (R12).  Vectors sized N_coarse / N_fine. */
 sfmg_status sfmg_prolong(sfmg_level coarse, sfmg_level fine, const double* d_uc, double* d_uf,

@@ -92,4 +92,28 @@ std::vector<double> make_interp(int pc, int pf) {
   return I;
 }
 
+// h-transfer at one order (NEXT-4; eq. (7) across nested meshes, R25): child s (0 = lower, 1 =
+// upper half) of a coarse element; H[i*n + a] = ell_a(xi_i), xi_i = (xhat_i + 2 s - 1) / 2 the
+// coarse-element coordinate of the child's node i.
+std::vector<double> make_h_interp(int p, int s) {
+  Basis1D B = make_basis(p);
+  const int n = B.n;
+  std::vector<double> lam(n, 1.0);
+  for (int j = 0; j < n; ++j)
+    for (int k = 0; k < n; ++k)
+      if (k != j) lam[j] /= (B.x[j] - B.x[k]);
+  std::vector<double> H(n * n, 0.0);
+  for (int i = 0; i < n; ++i) {
+    const double t = 0.5 * (B.x[i] + 2.0 * s - 1.0);
+    int hit = -1;
+    for (int a = 0; a < n; ++a)
+      if (t == B.x[a]) hit = a;
+    if (hit >= 0) { H[i * n + hit] = 1.0; continue; }
+    double den = 0.0;
+    for (int a = 0; a < n; ++a) den += lam[a] / (t - B.x[a]);
+    for (int a = 0; a < n; ++a) H[i * n + a] = (lam[a] / (t - B.x[a])) / den;
+  }
+  return H;
+}
+
 }  // namespace sfmg

@@ -133,6 +133,51 @@ __global__ void k_pcg_xr(RedScratch r, double* x, double* rv, const double* __re
   if (grid_reduce<1>(v, r, f)) r.scalars[slot] = f[0];
 }
 
+// General coarse CG (any order; R13), flag-gated so that batches of iterations can be queued and the
+// host polls only between batches.  Scalar slots (kCgc*): ||b||^2, rho = ||r||^2, (p, q), ||r_new||^2,
+// beta, flag (0 running, 1 converged, 2 breakdown, 3 max_iter), iterations.  Every block reads the
+// same flag / (p, q) at kernel start, so an early return is uniform and never leaves grid_reduce's
+// block counter half-counted.
+__global__ void k_cgc_start(double* scal) {
+  scal[kCgcIt] = 0.0;
+  scal[kCgcRho] = scal[kCgcBB];
+  scal[kCgcFlag] = (scal[kCgcBB] > 0.0) ? 0.0 : 1.0;
+}
+
+__global__ void k_cgc_xr(RedScratch r, double* x, double* rv, const double* __restrict__ p,
+                         const double* __restrict__ q, long long n) {
+  const double flag = r.scalars[kCgcFlag], pq = r.scalars[kCgcPQ];
+  if (flag != 0.0 || !(pq > 0.0)) return;
+  const double alpha = r.scalars[kCgcRho] / pq;
+  double v[1] = {0.0};
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    x[i] += alpha * p[i];
+    const double ri = rv[i] - alpha * q[i];
+    rv[i] = ri;
+    v[0] += ri * ri;
+  }
+  double f[1];
+  if (grid_reduce<1>(v, r, f)) r.scalars[kCgcRn] = f[0];
+}
+
+__global__ void k_cgc_check(double* scal, double rtol, int maxit) {
+  if (scal[kCgcFlag] != 0.0) return;
+  if (!(scal[kCgcPQ] > 0.0)) { scal[kCgcFlag] = 2.0; return; }
+  const double rn = scal[kCgcRn];
+  scal[kCgcBeta] = rn / scal[kCgcRho];
+  scal[kCgcRho] = rn;
+  scal[kCgcIt] += 1.0;
+  if (sqrt(rn) <= rtol * sqrt(scal[kCgcBB])) scal[kCgcFlag] = 1.0;
+  else if (scal[kCgcIt] >= (double)maxit) scal[kCgcFlag] = 3.0;
+}
+
+__global__ void k_cgc_p(const double* __restrict__ scal, double* p, const double* __restrict__ r, long long n) {
+  if (scal[kCgcFlag] != 0.0) return;
+  const double beta = scal[kCgcBeta];
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    p[i] = r[i] + beta * p[i];
+}
+
 __global__ void k_pcg_p(const double* __restrict__ scal, double* p, const double* __restrict__ z, int ia, int ib,
                         long long n) {
   const double beta = scal[ia] / scal[ib];
@@ -247,6 +292,18 @@ cudaError_t launch_scale_mul(double a, const double* x, const double* d, double*
 }
 cudaError_t launch_axpy1(double* x, const double* y, long long n, cudaStream_t s) {
   k_axpy1<<<vgrid(n), 256, 0, s>>>(x, y, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cgc_start(const RedScratch& red, cudaStream_t s) {
+  k_cgc_start<<<1, 1, 0, s>>>(red.scalars);
+  return cudaGetLastError();
+}
+cudaError_t launch_cgc_iter_tail(const RedScratch& red, double* x, double* r, double* p, const double* q, long long n,
+                                 double rtol, int maxit, cudaStream_t s) {
+  k_cgc_xr<<<kRedBlocks, kRedThreads, 0, s>>>(red, x, r, p, q, n);
+  k_cgc_check<<<1, 1, 0, s>>>(red.scalars, rtol, maxit);
+  k_cgc_p<<<vgrid(n), 256, 0, s>>>(red.scalars, p, r, n);
   return cudaGetLastError();
 }
 

@@ -297,4 +297,200 @@ cudaError_t launch_restrict_h(const MeshDev& mc, const MeshDev& mf, const double
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------------------------------
+// h-transfer at any order p (NEXT-4: "high-order restriction and prolongation").  Fine
+// element (ex, ey, ez) is child (ex & 1, ey & 1, ez & 1) of coarse element (ex/2, ey/2, ez/2), so
+// per element P is the tensor contraction u_f(i,j,k) = sum_{abc} H_sx[i][a] H_sy[j][b] H_sz[k][c]
+// u_c(a,b,c) with the child matrices H_s = make_h_interp(p, s) -- the same sum-factorised x, y, z
+// passes as the p-transfer; canonical owners write (prolong), restriction is the exact transpose
+// with fp64 REDs into the coarse element.  P0 = M_f P M_c (R12).
+
+constexpr int hOffset(int P) {
+  int s = 0;
+  for (int q = 1; q < P; ++q) s += 2 * (q + 1) * (q + 1);
+  return s;
+}
+__constant__ double c_H[hOffset(17)];   // per order: H_0 then H_1, [i][a]
+static bool g_h_uploaded[17];
+
+cudaError_t upload_h_tables(int p) {
+  if (p < 1 || p > 16) return cudaErrorInvalidValue;
+  if (g_h_uploaded[p]) return cudaSuccess;
+  const int n = p + 1;
+  for (int sc = 0; sc < 2; ++sc) {
+    std::vector<double> H = make_h_interp(p, sc);
+    cudaError_t e = cudaMemcpyToSymbol(c_H, H.data(), sizeof(double) * n * n, sizeof(double) * (hOffset(p) + sc * n * n));
+    if (e) return e;
+  }
+  g_h_uploaded[p] = true;
+  return cudaSuccess;
+}
+
+template <int P>
+__device__ __forceinline__ double hmat(int s, int i, int a) {
+  return c_H[hOffset(P) + s * (P + 1) * (P + 1) + i * (P + 1) + a];
+}
+
+template <int P>
+__global__ void __launch_bounds__(256) k_prolong_hp(MeshDev mc, MeshDev mf, const double* __restrict__ uc,
+                                                    double* __restrict__ uf, int add) {
+  constexpr int N = P + 1, N2 = N * N, N3 = N2 * N;
+  extern __shared__ double sm[];
+  double* sc = sm;        // [c][b][a]
+  double* t1 = sc + N3;   // [c][b][i]
+  double* t2 = t1 + N3;   // [c][j][i]
+  const long long e = blockIdx.x;
+  int ex, ey, ez;
+  ecoords(mf, e, ex, ey, ez);
+  const int sx = ex & 1, sy = ey & 1, sz = ez & 1;
+  const int cx = ex >> 1, cy = ey >> 1, cz = ez >> 1;
+  for (int l = threadIdx.x; l < N3; l += blockDim.x) {
+    const int a = l % N, b = (l / N) % N, c = l / N2;
+    const int I0 = cx * P + a, J0 = cy * P + b, K0 = cz * P + c;
+    const bool bnd = I0 == 0 || I0 == mc.Mx - 1 || J0 == 0 || J0 == mc.My - 1 || K0 == 0 || K0 == mc.Mz - 1;
+    sc[l] = bnd ? 0.0 : uc[I0 + (long long)mc.Mx * (J0 + (long long)mc.My * K0)];
+  }
+  __syncthreads();
+  for (int l = threadIdx.x; l < N3; l += blockDim.x) {
+    const int i = l % N, r = l / N;
+    double s = 0.0;
+#pragma unroll
+    for (int a = 0; a < N; ++a) s += hmat<P>(sx, i, a) * sc[a + N * r];
+    t1[l] = s;
+  }
+  __syncthreads();
+  for (int l = threadIdx.x; l < N3; l += blockDim.x) {
+    const int i = l % N, j = (l / N) % N, c = l / N2;
+    double s = 0.0;
+#pragma unroll
+    for (int b = 0; b < N; ++b) s += hmat<P>(sy, j, b) * t1[i + N * (b + N * c)];
+    t2[l] = s;
+  }
+  __syncthreads();
+  for (int l = threadIdx.x; l < N3; l += blockDim.x) {
+    const int i = l % N, j = (l / N) % N, k = l / N2;
+    if ((i == 0 && ex > 0) || (j == 0 && ey > 0) || (k == 0 && ez > 0)) continue;   // not the owner
+    const int I0 = ex * P + i, J0 = ey * P + j, K0 = ez * P + k;
+    const bool bnd = I0 == 0 || I0 == mf.Mx - 1 || J0 == 0 || J0 == mf.My - 1 || K0 == 0 || K0 == mf.Mz - 1;
+    const long long g = I0 + (long long)mf.Mx * (J0 + (long long)mf.My * K0);
+    if (bnd) {
+      if (!add) uf[g] = 0.0;
+      continue;
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int c = 0; c < N; ++c) s += hmat<P>(sz, k, c) * t2[i + N * (j + N * c)];
+    if (add) uf[g] += s; else uf[g] = s;
+  }
+}
+
+template <int P>
+__global__ void __launch_bounds__(256) k_restrict_hp(MeshDev mc, MeshDev mf, const double* __restrict__ rf,
+                                                     double* __restrict__ rc) {
+  constexpr int N = P + 1, N2 = N * N, N3 = N2 * N;
+  extern __shared__ double sm[];
+  double* sf = sm;        // [k][j][i]
+  double* t1 = sf + N3;   // [k][j][a]
+  double* t2 = t1 + N3;   // [k][b][a]
+  const long long e = blockIdx.x;
+  int ex, ey, ez;
+  ecoords(mf, e, ex, ey, ez);
+  const int sx = ex & 1, sy = ey & 1, sz = ez & 1;
+  const int cx = ex >> 1, cy = ey >> 1, cz = ez >> 1;
+  for (int l = threadIdx.x; l < N3; l += blockDim.x) {
+    const int i = l % N, j = (l / N) % N, k = l / N2;
+    double v = 0.0;
+    if (!((i == 0 && ex > 0) || (j == 0 && ey > 0) || (k == 0 && ez > 0))) {
+      const int I0 = ex * P + i, J0 = ey * P + j, K0 = ez * P + k;
+      const bool bnd = I0 == 0 || I0 == mf.Mx - 1 || J0 == 0 || J0 == mf.My - 1 || K0 == 0 || K0 == mf.Mz - 1;
+      if (!bnd) v = rf[I0 + (long long)mf.Mx * (J0 + (long long)mf.My * K0)];
+    }
+    sf[l] = v;
+  }
+  __syncthreads();
+  for (int l = threadIdx.x; l < N3; l += blockDim.x) {
+    const int a = l % N, r = l / N;
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) s += hmat<P>(sx, i, a) * sf[i + N * r];
+    t1[l] = s;
+  }
+  __syncthreads();
+  for (int l = threadIdx.x; l < N3; l += blockDim.x) {
+    const int a = l % N, b = (l / N) % N, k = l / N2;
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j) s += hmat<P>(sy, j, b) * t1[a + N * (j + N * k)];
+    t2[l] = s;
+  }
+  __syncthreads();
+  for (int l = threadIdx.x; l < N3; l += blockDim.x) {
+    const int a = l % N, b = (l / N) % N, c = l / N2;
+    const int I0 = cx * P + a, J0 = cy * P + b, K0 = cz * P + c;
+    const bool bnd = I0 == 0 || I0 == mc.Mx - 1 || J0 == 0 || J0 == mc.My - 1 || K0 == 0 || K0 == mc.Mz - 1;
+    if (bnd) continue;
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < N; ++k) s += hmat<P>(sz, k, c) * t2[a + N * (b + N * k)];
+    atomicAdd(rc + I0 + (long long)mc.Mx * (J0 + (long long)mc.My * K0), s);
+  }
+}
+
+template <int P>
+static cudaError_t prolong_hp_p(const MeshDev& mc, const MeshDev& mf, const double* uc, double* uf, int add,
+                                cudaStream_t s) {
+  constexpr size_t smem = sizeof(double) * 3 * (P + 1) * (P + 1) * (P + 1);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_prolong_hp<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e) return e;
+    attr = true;
+  }
+  k_prolong_hp<P><<<(unsigned)mf.E, 256, smem, s>>>(mc, mf, uc, uf, add);
+  return cudaGetLastError();
+}
+
+template <int P>
+static cudaError_t restrict_hp_p(const MeshDev& mc, const MeshDev& mf, const double* rf, double* rc, cudaStream_t s) {
+  constexpr size_t smem = sizeof(double) * 3 * (P + 1) * (P + 1) * (P + 1);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_restrict_hp<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e) return e;
+    attr = true;
+  }
+  cudaError_t e = cudaMemsetAsync(rc, 0, sizeof(double) * mc.N, s);
+  if (e) return e;
+  k_restrict_hp<P><<<(unsigned)mf.E, 256, smem, s>>>(mc, mf, rf, rc);
+  return cudaGetLastError();
+}
+
+#define SFMG_HP_CASES(F, ...)                                                             \
+  switch (mf.p) {                                                                         \
+    case 1: return F<1>(__VA_ARGS__);   case 2: return F<2>(__VA_ARGS__);                 \
+    case 3: return F<3>(__VA_ARGS__);   case 4: return F<4>(__VA_ARGS__);                 \
+    case 5: return F<5>(__VA_ARGS__);   case 6: return F<6>(__VA_ARGS__);                 \
+    case 7: return F<7>(__VA_ARGS__);   case 8: return F<8>(__VA_ARGS__);                 \
+    case 9: return F<9>(__VA_ARGS__);   case 10: return F<10>(__VA_ARGS__);               \
+    case 11: return F<11>(__VA_ARGS__); case 12: return F<12>(__VA_ARGS__);               \
+    case 13: return F<13>(__VA_ARGS__); case 14: return F<14>(__VA_ARGS__);               \
+    case 15: return F<15>(__VA_ARGS__); case 16: return F<16>(__VA_ARGS__);               \
+  }                                                                                       \
+  return cudaErrorInvalidValue;
+
+cudaError_t launch_prolong_hp(const MeshDev& mc, const MeshDev& mf, const double* uc, double* uf, int add,
+                              cudaStream_t s) {
+  if (mc.p != mf.p) return cudaErrorInvalidValue;
+  cudaError_t e = upload_h_tables(mf.p);
+  if (e) return e;
+  SFMG_HP_CASES(prolong_hp_p, mc, mf, uc, uf, add, s)
+}
+
+cudaError_t launch_restrict_hp(const MeshDev& mc, const MeshDev& mf, const double* rf, double* rc, cudaStream_t s) {
+  if (mc.p != mf.p) return cudaErrorInvalidValue;
+  cudaError_t e = upload_h_tables(mf.p);
+  if (e) return e;
+  SFMG_HP_CASES(restrict_hp_p, mc, mf, rf, rc, s)
+}
+
 }  // namespace sfmg

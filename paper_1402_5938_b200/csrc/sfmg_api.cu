@@ -569,10 +569,11 @@ sfmg_status sfmg_cheb_host(sfmg_level lv, const double* h_b, double* h_x, int64_
   return SFMG_OK;
 }
 
-// 1: p pair (fine.p = 2 coarse.p <= 16, same element grid); 2: h pair (p = 1 both, fine ne = 2 coarse ne)
+// 1: p pair (fine.p = 2 coarse.p <= 16, same element grid); 2: h pair (same p, fine ne = 2 coarse ne;
+// p = 1: NEXT-1 trilinear gathers, p > 1: NEXT-4 high-order h-transfer)
 static int pair_kind(const MeshDev& c, const MeshDev& f) {
   if (f.p == 2 * c.p && c.p <= 8 && f.nex == c.nex && f.ney == c.ney && f.nez == c.nez) return 1;
-  if (c.p == 1 && f.p == 1 && f.nex == 2 * c.nex && f.ney == 2 * c.ney && f.nez == 2 * c.nez) return 2;
+  if (c.p == f.p && f.nex == 2 * c.nex && f.ney == 2 * c.ney && f.nez == 2 * c.nez) return 2;
   return 0;
 }
 
@@ -580,7 +581,7 @@ static sfmg_status check_pair(sfmg_level c, sfmg_level f, int* kind) {
   if (!c || !f) return SFMG_E_ARG;
   *kind = pair_kind(c->m, f->m);
   if (!*kind) {
-    set_error("levels are neither (p/2, p) on one element grid nor (ne/2, ne) at p = 1");
+    set_error("levels are neither (p/2, p) on one element grid nor (ne/2, ne) at one order");
     return SFMG_E_PCOARSEN;
   }
   return SFMG_OK;
@@ -588,11 +589,14 @@ static sfmg_status check_pair(sfmg_level c, sfmg_level f, int* kind) {
 
 static cudaError_t transfer_prolong(const MeshDev& c, const MeshDev& f, const double* uc, double* uf, int add,
                                     cudaStream_t s) {
-  return pair_kind(c, f) == 2 ? launch_prolong_h(c, f, uc, uf, add, s) : launch_prolong(c, f, uc, uf, add, s);
+  if (pair_kind(c, f) == 2)
+    return f.p == 1 ? launch_prolong_h(c, f, uc, uf, add, s) : launch_prolong_hp(c, f, uc, uf, add, s);
+  return launch_prolong(c, f, uc, uf, add, s);
 }
 static cudaError_t transfer_restrict(const MeshDev& c, const MeshDev& f, const double* rf, double* rc,
                                      cudaStream_t s) {
-  return pair_kind(c, f) == 2 ? launch_restrict_h(c, f, rf, rc, s) : launch_restrict(c, f, rf, rc, s);
+  if (pair_kind(c, f) == 2) return f.p == 1 ? launch_restrict_h(c, f, rf, rc, s) : launch_restrict_hp(c, f, rf, rc, s);
+  return launch_restrict(c, f, rf, rc, s);
 }
 
 sfmg_status sfmg_prolong(sfmg_level coarse, sfmg_level fine, const double* d_uc, double* d_uf, void* stream) {
@@ -618,14 +622,15 @@ sfmg_status sfmg_restrict(sfmg_level coarse, sfmg_level fine, const double* d_rf
 // ------------------------------------------------------------------------------ hierarchy
 
 // Level problems of the hierarchy: orders p, p/2, ..., 1 on the fine mesh, then
-// mg->h_levels p = 1 levels on meshes ne/2, ne/4, ....
+// mg->h_levels p = 1 levels on meshes ne/2, ne/4, ....  mg->coarsen = 1
+// (NEXT-4, high-order h-multigrid): order p on meshes ne, ne/2, ..., ne/2^h_levels.
 static sfmg_status hier_specs(const sfmg_problem* fine, const sfmg_mg_params* mg, std::vector<sfmg_problem>& out) {
   out.clear();
   for (int q = fine->order;; q /= 2) {
     sfmg_problem pr = *fine;
     pr.order = q;
     out.push_back(pr);
-    if (q == 1) break;
+    if (q == 1 || mg->coarsen == 1) break;
     if (q % 2) { set_error("order cannot be p-coarsened to 1 by halving"); return SFMG_E_PCOARSEN; }
   }
   for (int j = 1; j <= mg->h_levels; ++j) {
@@ -645,7 +650,8 @@ static sfmg_status check_mg(const sfmg_mg_params* mg) {
       !(mg->eig_lo_frac > 0) || mg->power_iters < 1 || !(mg->coarse_rtol > 0) || mg->coarse_max_iter < 1 ||
       (mg->smoother != 0 && mg->smoother != 1) || (mg->smoother == 1 && !(mg->jacobi_omega > 0 && mg->jacobi_omega < 2)) ||
       (mg->lambda_method != 0 && mg->lambda_method != 1) || (mg->lambda_method == 1 && mg->power_iters > 16) ||
-      mg->h_levels < 0 || mg->h_levels > 20) {
+      mg->h_levels < 0 || mg->h_levels > 20 || (mg->coarsen != 0 && mg->coarsen != 1) ||
+      (mg->coarsen == 1 && mg->h_levels < 1)) {
     set_error("bad multigrid parameters");
     return SFMG_E_ARG;
   }
@@ -724,6 +730,14 @@ sfmg_status sfmg_hier_create(const sfmg_problem* fine, const sfmg_mg_params* mg,
       cudaError_t e = upload_interp_tables(q.order / 2, s);
       if (e) { sfmg_hier_destroy(h); return cuda_fail(e, "interp tables"); }
     }
+    if (l + 1 < specs.size() && specs[l + 1].order == q.order && q.order > 1) {
+      cudaError_t e = upload_h_tables(q.order);
+      if (e) { sfmg_hier_destroy(h); return cuda_fail(e, "h tables"); }
+    }
+  }
+  {
+    const MeshDev& mc = h->lv.back()->m;
+    h->host_coarse = !((mc.p == 1 || mc.p == 2));   // single-CTA device CG only for p <= 2 coarse levels
   }
   h->lam.assign(h->lv.size(), 0.0);
   for (size_t l = 0; l + 1 < h->lv.size(); ++l) {
@@ -760,11 +774,43 @@ sfmg_status sfmg_hier_lambda(sfmg_hier h, int32_t l, double* lam) {
 
 namespace sfmg {
 
+// Coarse solve of a level whose order is > 2 (high-order h-multigrid, NEXT-4): unpreconditioned CG
+// (R13) on the level's own apply and reduction kernels, x0 = 0, ||r|| <= rtol ||b||.  Convergence is
+// decided on the device after every iteration (a flag then freezes x, r, p); the iterations are
+// queued in batches of kCgcBatch and the host reads the flag between batches (syncs).
+static constexpr int kCgcBatch = 8;
+
+static cudaError_t coarse_cg_any(sfmg_level_s* lv, const double* b, double* x, double* r, double rtol, int maxit,
+                                 cudaStream_t s) {
+  const long long N = lv->N;
+  double* p = lv->t0;
+  double* q = lv->t1;
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(x, 0, sizeof(double) * N, s))) return e;
+  if ((e = launch_copy(b, r, N, s))) return e;
+  if ((e = launch_copy(b, p, N, s))) return e;
+  if ((e = launch_dot(lv->red, b, b, N, kCgcBB, s))) return e;
+  if ((e = launch_cgc_start(lv->red, s))) return e;
+  double flag = 0.0;
+  for (int it = 0; it < maxit; it += kCgcBatch) {
+    for (int k = 0; k < kCgcBatch; ++k) {
+      if ((e = op_apply(lv, 0, p, q, s))) return e;
+      if ((e = launch_dot(lv->red, p, q, N, kCgcPQ, s))) return e;
+      if ((e = launch_cgc_iter_tail(lv->red, x, r, p, q, N, rtol, maxit, s))) return e;
+    }
+    if ((e = cudaMemcpyAsync(&flag, lv->red.scalars + kCgcFlag, sizeof(double), cudaMemcpyDeviceToHost, s))) return e;
+    if ((e = cudaStreamSynchronize(s))) return e;
+    if (flag != 0.0) break;
+  }
+  return cudaSuccess;
+}
+
 static cudaError_t vcycle_level(sfmg_hier_s* h, size_t l, const double* b, double* x, cudaStream_t s) {
   sfmg_level_s* lv = h->lv[l];
   const sfmg_mg_params& mg = h->mg;
   cudaError_t e;
   if (l + 1 == h->lv.size()) {
+    if (h->host_coarse) return coarse_cg_any(lv, b, x, h->r[l], mg.coarse_rtol, mg.coarse_max_iter, s);
     return launch_coarse_cg(lv->m, lv->G, b, x, lv->t0, lv->t1, lv->y, lv->red.scalars, mg.coarse_rtol,
                             mg.coarse_max_iter, s);
   }
@@ -799,7 +845,7 @@ static cudaError_t vcycle_level(sfmg_hier_s* h, size_t l, const double* b, doubl
 // later call launches the instantiated graph on the caller's stream.  SFMG_NO_GRAPH=1 disables it.
 static cudaError_t vcycle(sfmg_hier_s* h, const double* b, double* x, cudaStream_t s) {
   static const bool no_graph = getenv("SFMG_NO_GRAPH") && getenv("SFMG_NO_GRAPH")[0] == '1';
-  if (no_graph) return vcycle_level(h, 0, b, x, s);
+  if (no_graph || h->host_coarse) return vcycle_level(h, 0, b, x, s);   // host-polled coarse CG: eager
   if (h->vc_exec && h->vc_b == b && h->vc_x == x) {
     h->fine_applies += h->vc_fine_applies;
     return cudaGraphLaunch(h->vc_exec, s);

@@ -12,6 +12,8 @@ namespace sfmg {
 constexpr int kMaxOrder = 16;
 constexpr int kRedBlocks = 592;   // 4 x 148 SMs: fixed grid of the deterministic reductions
 constexpr int kRedSlots = 4;      // partial sums per reduction pass
+// scalar slots of the general (flag-gated) coarse CG
+constexpr int kCgcBB = 20, kCgcRho = 21, kCgcPQ = 22, kCgcRn = 23, kCgcBeta = 24, kCgcFlag = 25, kCgcIt = 26;
 
 // Mesh + problem description passed by value to kernels.
 struct MeshDev {
@@ -42,6 +44,8 @@ struct Basis1D {
 Basis1D make_basis(int p);
 // I[i*(pc+1)+a] = ell^{pc}_a(x^{pf}_i)
 std::vector<double> make_interp(int pc, int pf);
+// h-transfer at order p, child s in {0, 1}: H[i*(p+1)+a] = ell_a((xhat_i + 2 s - 1) / 2)
+std::vector<double> make_h_interp(int p, int s);
 
 }  // namespace sfmg
 
@@ -85,6 +89,7 @@ struct sfmg_hier_s {
   double* vc_x = nullptr;
   int64_t vc_fine_applies = 0;
   int vc_eager_runs = 0;
+  bool host_coarse = false;   // coarsest order > 2: host-polled multi-kernel CG, V-cycle not captured
 };
 
 namespace sfmg {
@@ -143,6 +148,11 @@ cudaError_t launch_pcg_xr(const RedScratch& red, double* x, double* r, const dou
 // p = z + (scal[ia] / scal[ib]) p
 cudaError_t launch_pcg_p(const RedScratch& red, double* p, const double* z, int ia, int ib, long long n,
                          cudaStream_t s);
+// general coarse CG (any order; R13): start (it = 0, rho = ||b||^2, flag), and the tail of one
+// iteration after q = A p and (p, q) -> scalars[kCgcPQ]: x += a p, r -= a q, check, p = r + beta p
+cudaError_t launch_cgc_start(const RedScratch& red, cudaStream_t s);
+cudaError_t launch_cgc_iter_tail(const RedScratch& red, double* x, double* r, double* p, const double* q, long long n,
+                                 double rtol, int maxit, cudaStream_t s);
 // x += y
 cudaError_t launch_axpy1(double* x, const double* y, long long n, cudaStream_t s);
 // scalars[slot] = sum a b / dinv  (<a, b>_D, Arnoldi R26)
@@ -165,6 +175,11 @@ cudaError_t launch_restrict(const MeshDev& mc, const MeshDev& mf, const double* 
 cudaError_t launch_prolong_h(const MeshDev& mc, const MeshDev& mf, const double* uc, double* uf, int add,
                              cudaStream_t s);
 cudaError_t launch_restrict_h(const MeshDev& mc, const MeshDev& mf, const double* rf, double* rc, cudaStream_t s);
+// h pair at any order p = 1..16 (NEXT-4): same contract, block per fine element, sum-factorised
+cudaError_t upload_h_tables(int p);
+cudaError_t launch_prolong_hp(const MeshDev& mc, const MeshDev& mf, const double* uc, double* uf, int add,
+                              cudaStream_t s);
+cudaError_t launch_restrict_hp(const MeshDev& mc, const MeshDev& mf, const double* rf, double* rc, cudaStream_t s);
 
 void set_error(const std::string& s);
 

@@ -45,7 +45,7 @@ class _MgParams(C.Structure):
                 ("eig_lo_frac", C.c_double), ("eig_hi_frac", C.c_double), ("power_iters", C.c_int32),
                 ("power_seed", C.c_uint64), ("coarse_rtol", C.c_double), ("coarse_max_iter", C.c_int32),
                 ("smoother", C.c_int32), ("jacobi_omega", C.c_double), ("lambda_method", C.c_int32),
-                ("h_levels", C.c_int32)]
+                ("h_levels", C.c_int32), ("coarsen", C.c_int32)]
 
 
 class _Report(C.Structure):
@@ -319,6 +319,7 @@ class MgParams:
     jacobi_omega: float = 2.0 / 3.0
     lambda_method: int = 0
     h_levels: int = 0
+    coarsen: int = 0   # 1: high-order h-multigrid at fixed p (NEXT-4)
 
     @staticmethod
     def paper(smoother="cheb", h_levels=2):
@@ -331,10 +332,18 @@ class MgParams:
         return MgParams(nu_pre=1, nu_post=1, cheb_degree=3, eig_lo_frac=0.25, eig_hi_frac=1.0, lambda_method=1,
                         h_levels=h_levels)
 
+    @staticmethod
+    def paper_h(smoother="cheb", h_levels=2):
+        """The paper's h-multigrid columns: the same smoothers on three meshes
+        ne, ne/2, ne/4 at the fine order (NEXT-4)."""
+        mg = MgParams.paper(smoother, h_levels)
+        mg.coarsen = 1
+        return mg
+
     def _c(self):
         return _MgParams(self.nu_pre, self.nu_post, self.cheb_degree, self.eig_lo_frac, self.eig_hi_frac,
                          self.power_iters, self.power_seed, self.coarse_rtol, self.coarse_max_iter,
-                         self.smoother, self.jacobi_omega, self.lambda_method, self.h_levels)
+                         self.smoother, self.jacobi_omega, self.lambda_method, self.h_levels, self.coarsen)
 
 
 class Hierarchy:

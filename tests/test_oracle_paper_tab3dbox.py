@@ -14,24 +14,26 @@ import numpy as np
 import pytest
 
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "tab_3d_box.txt")
+GOLDEN_H = os.path.join(os.path.dirname(__file__), "golden", "tab_3d_box_h.txt")
 
 
-def paper_rows():
+def paper_rows(path=GOLDEN):
     rows = {}
-    for line in open(GOLDEN):
+    for line in open(path):
         if line.strip() and not line.startswith("#"):
             v = [int(t) for t in line.split()]
             rows[v[0]] = v[1:]
     return rows
 
 
-def counts(orc, p):
+def counts(orc, p, coarsen=0):
     out = []
     for mode in (0, 1):
         for sm in (1, 0):
             nu = 3 if sm == 1 else 1
             H = orc.Hier(8, 8, 8, p, nu_pre=nu, nu_post=nu, degree=3, lo_frac=0.25, hi_frac=1.0, power_iters=10,
-                         smoother=sm, omega=2.0 / 3.0, lambda_method=1, h_levels=2, geom_tier=2, tier=2)
+                         smoother=sm, omega=2.0 / 3.0, lambda_method=1, h_levels=2, geom_tier=2, tier=2,
+                         coarsen=coarsen)
             b = H.levels[0].load_vector(1)
             r = H.solve(b, mode=mode, rtol=1e-8, maxit=200)
             assert r["converged"]
@@ -47,6 +49,20 @@ def test_tab_3d_box_gauss_quadrature(orc, p):
     finally:
         orc.set_quadrature(0)
     paper = paper_rows()[p]
+    assert np.all(np.abs(np.array(ours) - np.array(paper)) <= 1), (p, ours, paper)
+
+
+@pytest.mark.parametrize("p", [1, 2, 3])
+def test_tab_3d_box_h_columns_gauss_quadrature(orc, p):
+    """NEXT-4: the h-multigrid columns (three meshes 8^3 -> 4^3 -> 2^3 at order p, P:1035-1041,
+    tests/golden/tab_3d_box_h.txt) agree to +-1 as well (p = 4 gives the printed 11, 8, 7, 6 exactly;
+    not run here to keep the CPU suite short)."""
+    orc.set_quadrature(1)
+    try:
+        ours = counts(orc, p, coarsen=1)
+    finally:
+        orc.set_quadrature(0)
+    paper = paper_rows(GOLDEN_H)[p]
     assert np.all(np.abs(np.array(ours) - np.array(paper)) <= 1), (p, ours, paper)
 
 
