@@ -1,6 +1,10 @@
 """Per-section split of an ncu report (source page): executed instructions and warp-stall samples
 between consecutive block barriers / mbarrier waits of a kernel.  Developer tool:
 python tools/ncu_sections.py report.ncu-rep"""
+import csv
+import subprocess
+import sys
+
 path = sys.argv[1]
 out = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "sass"], capture_output=True, text=True).stdout
 rows = list(csv.reader(out.splitlines()))
