@@ -106,6 +106,41 @@ def lib():
         L.orc_vcycle.argtypes = [vp, vp, vp]
         L.orc_solve.argtypes = [vp, i, vp, vp, d, i, C.POINTER(C.c_int), C.POINTER(C.c_int),
                                 dp, dp, vp, i, C.POINTER(C.c_int64)]
+        # NEXT-2: 2-D levels / hierarchies
+        L.orc2_level_create.restype = vp
+        L.orc2_level_create.argtypes = [i, i, i, i, d, i, d, d]
+        for nm in ("orc2_level_destroy", "orc2_hier_destroy"):
+            getattr(L, nm).argtypes = [vp]
+        L.orc2_level_status.argtypes = [vp]
+        L.orc2_level_ndofs.argtypes = [vp]
+        L.orc2_level_ndofs.restype = i64
+        L.orc2_mask.argtypes = [vp, vp]
+        L.orc2_geometry.argtypes = [vp, i64, vp]
+        L.orc2_element_matrix.argtypes = [vp, i64, vp]
+        L.orc2_assemble_dense.argtypes = [vp, i, vp]
+        L.orc2_apply.argtypes = [vp, i, vp, vp]
+        L.orc2_diag.argtypes = [vp, i, vp]
+        L.orc2_lambda_max.argtypes = [vp, i, u64]
+        L.orc2_lambda_max.restype = d
+        L.orc2_lambda_arnoldi.argtypes = [vp, i, u64]
+        L.orc2_lambda_arnoldi.restype = d
+        L.orc2_cheb.argtypes = [vp, vp, vp, i, d, d]
+        L.orc2_jacobi.argtypes = [vp, vp, vp, i, d]
+        L.orc2_prolong.argtypes = [vp, vp, vp, vp]
+        L.orc2_restrict.argtypes = [vp, vp, vp, vp]
+        L.orc2_load_vector.argtypes = [vp, i, vp]
+        L.orc2_exact_solution.argtypes = [vp, vp]
+        L.orc2_hier_create.restype = vp
+        L.orc2_hier_create.argtypes = [i, i, i, i, d, i, d, d, i, i, i, d, d, i, u64, d, i, i, d, i, i, i,
+                                       C.POINTER(C.c_int)]
+        L.orc2_hier_nlevels.argtypes = [vp]
+        L.orc2_hier_level.argtypes = [vp, i]
+        L.orc2_hier_level.restype = vp
+        L.orc2_hier_lambda.argtypes = [vp, i]
+        L.orc2_hier_lambda.restype = d
+        L.orc2_vcycle.argtypes = [vp, vp, vp]
+        L.orc2_solve.argtypes = [vp, i, vp, vp, d, i, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                 dp, dp, vp, i, C.POINTER(C.c_int64)]
         _lib = L
     return _lib
 
@@ -405,6 +440,175 @@ class Hier:
         hist = np.zeros(hist_cap)
         st = lib().orc_solve(self.h, mode, _p(b), _p(x), rtol, maxit, C.byref(it), C.byref(conv),
                              C.byref(r0), C.byref(rn), _p(hist), hist_cap, C.byref(fa))
+        return dict(x=x, status=st, iterations=it.value, converged=bool(conv.value),
+                    r0_norm=r0.value, r_norm=rn.value, history=hist[:min(it.value + 1, hist_cap)],
+                    fine_applies=fa.value)
+
+
+# ----------------------------------------------------------------------------- NEXT-2: 2-D
+class Level2:
+    """2-D quadrilateral level (NEXT-2): nex x ney elements of order p on the unit square,
+    warp 1: x_i += amp sin(pi X) sin(pi Y); coeff 0 const c0, 1 exp(c1 S), 2 10^(c1 S),
+    3 c0 + c1 (cos^2 2 pi x + cos^2 2 pi y) (2d-var), 4 the same with 10 pi (2d-var').  The quadrature
+    is the one set by set_quadrature() at creation."""
+
+    def __init__(self, nex, ney, p, warp=0, amp=0.0, coeff=0, c0=1.0, c1=0.0, _handle=None, _owner=None):
+        if _handle is None:
+            self.h = lib().orc2_level_create(nex, ney, p, warp, amp, coeff, c0, c1)
+            if not self.h:
+                raise ValueError("invalid level parameters")
+        else:
+            self.h, self._owner = _handle, _owner
+        self.nex, self.ney, self.p, self.n = nex, ney, p, p + 1
+        self.N = int(lib().orc2_level_ndofs(self.h))
+        self.E = nex * ney
+
+    def __del__(self):
+        try:
+            if self.h and getattr(self, "_owner", None) is None:
+                lib().orc2_level_destroy(self.h)
+            self.h = None
+        except Exception:
+            pass
+
+    @property
+    def status(self):
+        return int(lib().orc2_level_status(self.h))
+
+    def mask(self):
+        m = np.zeros(self.N, dtype=np.uint8)
+        lib().orc2_mask(self.h, m.ctypes.data_as(C.c_void_p))
+        return m
+
+    def geometry(self, e):
+        G = np.zeros(3 * self.n * self.n)
+        lib().orc2_geometry(self.h, e, _p(G))
+        return G.reshape(3, self.n * self.n)
+
+    def element_matrix(self, e):
+        K = np.zeros((self.n * self.n, self.n * self.n))
+        lib().orc2_element_matrix(self.h, e, _p(K))
+        return K
+
+    def assemble_dense(self, bc=0):
+        A = np.zeros((self.N, self.N))
+        lib().orc2_assemble_dense(self.h, bc, _p(A))
+        return A
+
+    def apply(self, u, bc=0):
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        v = np.zeros(self.N)
+        lib().orc2_apply(self.h, bc, _p(u), _p(v))
+        return v
+
+    def diag(self, bc=0):
+        d = np.zeros(self.N)
+        lib().orc2_diag(self.h, bc, _p(d))
+        return d
+
+    def lambda_max(self, iters=10, seed=12345):
+        return float(lib().orc2_lambda_max(self.h, iters, seed))
+
+    def lambda_arnoldi(self, m=10, seed=12345):
+        return float(lib().orc2_lambda_arnoldi(self.h, m, seed))
+
+    def cheb(self, b, x, degree, lo, hi):
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        x = np.array(x, dtype=np.float64)
+        lib().orc2_cheb(self.h, _p(b), _p(x), degree, lo, hi)
+        return x
+
+    def jacobi(self, b, x, steps, omega=2.0 / 3.0):
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        x = np.array(x, dtype=np.float64)
+        lib().orc2_jacobi(self.h, _p(b), _p(x), steps, omega)
+        return x
+
+    def load_vector(self, rhs_id=1):
+        f = np.zeros(self.N)
+        if lib().orc2_load_vector(self.h, rhs_id, _p(f)) != 0:
+            raise ValueError("unknown rhs")
+        return f
+
+    def exact_solution(self):
+        u = np.zeros(self.N)
+        lib().orc2_exact_solution(self.h, _p(u))
+        return u
+
+
+def prolong2(coarse: Level2, fine: Level2, uc):
+    uc = np.ascontiguousarray(uc, dtype=np.float64)
+    uf = np.zeros(fine.N)
+    if lib().orc2_prolong(coarse.h, fine.h, _p(uc), _p(uf)):
+        raise ValueError("levels are neither (p/2, p) on one grid nor (ne/2, ne) at one order")
+    return uf
+
+
+def restrict2(coarse: Level2, fine: Level2, rf):
+    rf = np.ascontiguousarray(rf, dtype=np.float64)
+    rc = np.zeros(coarse.N)
+    if lib().orc2_restrict(coarse.h, fine.h, _p(rf), _p(rc)):
+        raise ValueError("levels are neither (p/2, p) on one grid nor (ne/2, ne) at one order")
+    return rc
+
+
+class Hier2:
+    """2-D hierarchy (NEXT-2): coarsen 0 p-multigrid p, ..., 1 then h_levels meshes at p = 1; coarsen 1
+    high-order h-multigrid at order p (32x32, 16x16, 8x8)."""
+
+    def __init__(self, nex, ney, p, warp=0, amp=0.0, coeff=0, c0=1.0, c1=0.0, nu_pre=2, nu_post=2, degree=4,
+                 lo_frac=0.1, hi_frac=1.1, power_iters=10, seed=12345, coarse_rtol=1e-10, coarse_maxit=10000,
+                 smoother=0, omega=2.0 / 3.0, lambda_method=0, h_levels=0, coarsen=0):
+        st = C.c_int(0)
+        self.h = lib().orc2_hier_create(nex, ney, p, warp, amp, coeff, c0, c1, nu_pre, nu_post, degree, lo_frac,
+                                        hi_frac, power_iters, seed, coarse_rtol, coarse_maxit, smoother, omega,
+                                        lambda_method, h_levels, coarsen, C.byref(st))
+        self.status = st.value
+        if not self.h:
+            raise ValueError("cannot build hierarchy (status %d)" % st.value)
+        self.nlevels = int(lib().orc2_hier_nlevels(self.h))
+        orders, q = [], p
+        while True:
+            orders.append(q)
+            if q == 1 or coarsen == 1:
+                break
+            q //= 2
+        meshes = [(nex, ney)] * len(orders) + [(nex >> j, ney >> j) for j in range(1, h_levels + 1)]
+        orders += [orders[-1]] * h_levels
+        self.levels = [Level2(mx, my, q, _handle=lib().orc2_hier_level(self.h, l), _owner=self)
+                       for l, ((mx, my), q) in enumerate(zip(meshes, orders))]
+        self.N = self.levels[0].N
+
+    def __del__(self):
+        try:
+            if self.h:
+                for lv in self.levels:
+                    lv.h = None
+                lib().orc2_hier_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    def lam(self, l):
+        return float(lib().orc2_hier_lambda(self.h, l))
+
+    def vcycle(self, b):
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        x = np.zeros(self.N)
+        rc = lib().orc2_vcycle(self.h, _p(b), _p(x))
+        if rc:
+            raise RuntimeError("vcycle status %d" % rc)
+        return x
+
+    def solve(self, b, mode=1, rtol=1e-8, maxit=500, hist_cap=1024):
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        x = np.zeros(self.N)
+        it, conv = C.c_int(0), C.c_int(0)
+        r0, rn = C.c_double(0), C.c_double(0)
+        fa = C.c_int64(0)
+        hist = np.zeros(hist_cap)
+        st = lib().orc2_solve(self.h, mode, _p(b), _p(x), rtol, maxit, C.byref(it), C.byref(conv),
+                              C.byref(r0), C.byref(rn), _p(hist), hist_cap, C.byref(fa))
         return dict(x=x, status=st, iterations=it.value, converged=bool(conv.value),
                     r0_norm=r0.value, r_norm=rn.value, history=hist[:min(it.value + 1, hist_cap)],
                     fine_applies=fa.value)

@@ -529,7 +529,8 @@ double nrm2(const std::vector<double>& a) { return std::sqrt(dot(a, a)); }
 
 // R9: power iteration on D^{-1} A_D with the D-Rayleigh quotient; start = splitmix64(seed)
 // uniform in [-1,1], boundary zeroed; exactly `iters` applies.
-double lambda_max(Level& L, int iters, uint64_t seed, int64_t* applies) {
+template <class LV>
+double lambda_max(LV& L, int iters, uint64_t seed, int64_t* applies) {
   const std::vector<double>& d = level_diag(L);
   std::vector<double> x(L.N), y(L.N);
   for (int64_t g = 0; g < L.N; ++g) x[g] = L.boundary(g) ? 0.0 : uniform_pm1(seed, (uint64_t)g);
@@ -549,7 +550,8 @@ double lambda_max(Level& L, int iters, uint64_t seed, int64_t* applies) {
 
 // R7: Chebyshev acceleration of Jacobi on D^{-1}A_D over [lo, hi],
 // K steps = K applies, written in the residual / correction form.
-void chebyshev(Level& L, const double* b, double* x, int K, double lo, double hi, int64_t* applies) {
+template <class LV>
+void chebyshev(LV& L, const double* b, double* x, int K, double lo, double hi, int64_t* applies) {
   const std::vector<double>& d = level_diag(L);
   int64_t N = L.N;
   double theta = 0.5 * (hi + lo), delta = 0.5 * (hi - lo), sigma = theta / delta;
@@ -712,7 +714,8 @@ void transfer_restrict(const Level& C, const Level& F, const double* rf, double*
 
 // Damped point Jacobi, omega = 2/3 in the paper:
 // x <- x + omega D^{-1} (b - A_D x); one apply per step.
-void jacobi(Level& L, const double* b, double* x, int steps, double omega, int64_t* applies) {
+template <class LV>
+void jacobi(LV& L, const double* b, double* x, int steps, double omega, int64_t* applies) {
   const std::vector<double>& d = level_diag(L);
   std::vector<double> Ax(L.N);
   for (int s = 0; s < steps; ++s) {
@@ -756,7 +759,8 @@ void sym_eig_jacobi(int n, std::vector<double> A, std::vector<double>& ev) {
 // self-adjoint; start = splitmix64(seed) uniform in [-1,1] with the boundary zeroed (R9).  The
 // estimate is the largest eigenvalue of the k x k Hessenberg matrix H (k = m, or fewer on an
 // invariant subspace), symmetric tridiagonal up to rounding; its symmetric part is diagonalised.
-double lambda_arnoldi(Level& L, int m, uint64_t seed, int64_t* applies) {
+template <class LV>
+double lambda_arnoldi(LV& L, int m, uint64_t seed, int64_t* applies) {
   const std::vector<double>& d = level_diag(L);
   const int64_t N = L.N;
   auto dotD = [&](const std::vector<double>& a, const std::vector<double>& b) {
@@ -801,8 +805,9 @@ double lambda_arnoldi(Level& L, int m, uint64_t seed, int64_t* applies) {
 
 /* ------------------------------------------------------------------ hierarchy / solvers */
 
-struct Hier {
-  std::vector<Level*> lv;   // lv[0] finest (order p), lv.back() order 1
+template <class LV>
+struct HierT {
+  std::vector<LV*> lv;      // lv[0] finest (order p), lv.back() the coarsest level
   std::vector<double> lam;
   int nu_pre, nu_post, K;
   double lo_frac, hi_frac, coarse_rtol;
@@ -814,12 +819,15 @@ struct Hier {
   int64_t fine_applies = 0;
   int64_t coarse_iters_last = 0;
 };
+using Hier = HierT<Level>;
 
-int64_t* counter_for(Hier& H, int l) { return l == 0 ? &H.fine_applies : nullptr; }
+template <class H_>
+int64_t* counter_for(H_& H, int l) { return l == 0 ? &H.fine_applies : nullptr; }
 
 // R13: unpreconditioned CG on the coarsest level, x0 = 0, ||r|| <= rtol ||b||.
-int coarse_cg(Hier& H, const double* b, double* x) {
-  Level& L = *H.lv.back();
+template <class LV>
+int coarse_cg(HierT<LV>& H, const double* b, double* x) {
+  LV& L = *H.lv.back();
   int64_t N = L.N;
   int l = (int)H.lv.size() - 1;
   std::vector<double> r(b, b + N), p(b, b + N), Ap(N);
@@ -846,8 +854,9 @@ int coarse_cg(Hier& H, const double* b, double* x) {
 }
 
 // V-cycle from x = 0 (R11).
-int vcycle(Hier& H, int l, const double* b, double* x) {
-  Level& L = *H.lv[l];
+template <class LV>
+int vcycle(HierT<LV>& H, int l, const double* b, double* x) {
+  LV& L = *H.lv[l];
   int64_t N = L.N;
   if (l == (int)H.lv.size() - 1) return coarse_cg(H, b, x);
   for (int64_t g = 0; g < N; ++g) x[g] = 0.0;
@@ -862,7 +871,7 @@ int vcycle(Hier& H, int l, const double* b, double* x) {
   apply(L, 0, x, r.data(), L.tier);
   if (int64_t* c = counter_for(H, l)) ++*c;
   for (int64_t g = 0; g < N; ++g) r[g] = b[g] - r[g];
-  Level& C = *H.lv[l + 1];
+  LV& C = *H.lv[l + 1];
   std::vector<double> bc(C.N), ec(C.N), ef(N);
   transfer_restrict(C, L, r.data(), bc.data());
   int st = vcycle(H, l + 1, bc.data(), ec.data());
@@ -871,6 +880,361 @@ int vcycle(Hier& H, int l, const double* b, double* x) {
   for (int64_t g = 0; g < N; ++g) x[g] += ef[g];
   for (int s = 0; s < H.nu_post; ++s) smooth();
   return 0;
+}
+
+/* ================================================================== NEXT-2: 2-D quadrilaterals */
+// The 2-D problems of the paper: -div(mu grad u) = f on the unit square (2d-const) or a
+// warped square (2d-var, 2d-var'), with the same discretisation as in 3-D: tensor LGL
+// nodal basis of order p on quadrilaterals, isoparametric geometry, Gauss or collocated LGL
+// quadrature (R1 / NEXT-3).  Written separately from the 3-D level (no shared element code); the
+// smoothers, eigenvalue estimates, hierarchy and solvers above are templates over the level type.
+
+// mu in 2-D (R6): 0: c0 (2d-const); 1: exp(c1 S), 2: 10^(c1 S), S = sin 2 pi x sin 2 pi y;
+// 3: c0 + c1 (cos^2 2 pi x + cos^2 2 pi y) (2d-var, c0 = 1, c1 = 1e6); 4: c0 + c1 (cos^2 10 pi x +
+// cos^2 10 pi y) (2d-var').
+double coeff_mu2(int kind, double c0, double c1, double x, double y) {
+  const double S = std::sin(2 * kPi * x) * std::sin(2 * kPi * y);
+  switch (kind) {
+    case 0: return c0;
+    case 1: return std::exp(c1 * S);
+    case 2: return std::pow(10.0, c1 * S);
+    case 3: { double a = std::cos(2 * kPi * x), b = std::cos(2 * kPi * y); return c0 + c1 * (a * a + b * b); }
+    case 4: { double a = std::cos(10 * kPi * x), b = std::cos(10 * kPi * y); return c0 + c1 * (a * a + b * b); }
+  }
+  return NAN;
+}
+void coeff_grad2(int kind, double c0, double c1, double x, double y, double g[2]) {
+  const double dS[2] = {2 * kPi * std::cos(2 * kPi * x) * std::sin(2 * kPi * y),
+                        2 * kPi * std::sin(2 * kPi * x) * std::cos(2 * kPi * y)};
+  const double mu = coeff_mu2(kind, c0, c1, x, y);
+  switch (kind) {
+    case 0: g[0] = g[1] = 0.0; return;
+    case 1: g[0] = c1 * mu * dS[0]; g[1] = c1 * mu * dS[1]; return;
+    case 2: g[0] = std::log(10.0) * c1 * mu * dS[0]; g[1] = std::log(10.0) * c1 * mu * dS[1]; return;
+    case 3: g[0] = -2 * kPi * c1 * std::sin(4 * kPi * x); g[1] = -2 * kPi * c1 * std::sin(4 * kPi * y); return;
+    case 4: g[0] = -10 * kPi * c1 * std::sin(20 * kPi * x); g[1] = -10 * kPi * c1 * std::sin(20 * kPi * y); return;
+  }
+}
+
+struct Level2 {
+  int nex, ney, p, n, warp, coeff;
+  double amp, c0, c1;
+  int64_t E, N, Mx, My, n2;
+  int tier = 2;                    // (one apply tier in 2-D: direct quadrature)
+  Basis B;
+  std::vector<double> G;           // [E][3][n2] at the quadrature points: (00, 01, 11)
+  std::vector<double> detJ;        // [E][n2]
+  std::vector<double> diag_cache;
+  std::vector<std::vector<int64_t>> colour_elems;   // 4 colours, (ex & 1) | (ey & 1) << 1
+  double min_detj = 1e300;
+  int status = 0;
+  void elem_coords(int64_t e, int& ex, int& ey) const { ex = (int)(e % nex); ey = (int)(e / nex); }
+  int64_t l2g(int64_t e, int a, int b) const {
+    int ex, ey; elem_coords(e, ex, ey);
+    return ((int64_t)ex * p + a) + Mx * ((int64_t)ey * p + b);
+  }
+  bool boundary(int64_t g) const {
+    int64_t I = g % Mx, J = g / Mx;
+    return I == 0 || I == Mx - 1 || J == 0 || J == My - 1;
+  }
+};
+
+// Physical node coordinates of element e: reference-square point, then x_i += a sin(pi X) sin(pi Y)
+// (the 2-D analogue of the BASELINE warp; the paper's own warped square is unpublished, R5).
+void element_nodes2(const Level2& L, int64_t e, std::vector<double>& X) {
+  const int n = L.n;
+  X.assign(2 * L.n2, 0.0);
+  int ex, ey; L.elem_coords(e, ex, ey);
+  for (int b = 0; b < n; ++b)
+    for (int a = 0; a < n; ++a) {
+      const int l = a + n * b;
+      const double Xr = (ex + 0.5 * (L.B.x[a] + 1.0)) / L.nex, Yr = (ey + 0.5 * (L.B.x[b] + 1.0)) / L.ney;
+      const double s = (L.warp == 1) ? L.amp * std::sin(kPi * Xr) * std::sin(kPi * Yr) : 0.0;
+      X[l] = Xr + s; X[L.n2 + l] = Yr + s;
+    }
+}
+
+// grad_ref phi_(a,b) at quadrature point (i,j) from the 1-D tabulations.
+inline void grad_phi2(const Basis& B, int i, int j, int a, int b, double d[2]) {
+  const int n = B.n;
+  d[0] = B.dL[i * n + a] * B.L[j * n + b];
+  d[1] = B.L[i * n + a] * B.dL[j * n + b];
+}
+
+// G_q = w_i w_j mu(x_q) detJ_q J_q^{-1} J_q^{-T}, J = d x / d xi by the definition
+// J[al][be] = sum_l x_l^al d_be phi_l(xi_q).  Returns min det J.
+double element_geometry2(const Level2& L, int64_t e, double* G, double* dJ) {
+  const int n = L.n; const int64_t n2 = L.n2;
+  std::vector<double> X;
+  element_nodes2(L, e, X);
+  double mind = 1e300;
+  for (int j = 0; j < n; ++j)
+    for (int i = 0; i < n; ++i) {
+      const int q = i + n * j;
+      double J[2][2] = {{0, 0}, {0, 0}}, xq[2] = {0, 0};
+      for (int b = 0; b < n; ++b)
+        for (int a = 0; a < n; ++a) {
+          const int l = a + n * b;
+          double d[2];
+          grad_phi2(L.B, i, j, a, b, d);
+          for (int al = 0; al < 2; ++al)
+            for (int be = 0; be < 2; ++be) J[al][be] += X[al * n2 + l] * d[be];
+          const double ph = L.B.L[i * n + a] * L.B.L[j * n + b];
+          xq[0] += ph * X[l]; xq[1] += ph * X[n2 + l];
+        }
+      const double det = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+      mind = std::min(mind, det);
+      const double Ji[2][2] = {{J[1][1] / det, -J[0][1] / det}, {-J[1][0] / det, J[0][0] / det}};
+      const double s = L.B.qw[i] * L.B.qw[j] * coeff_mu2(L.coeff, L.c0, L.c1, xq[0], xq[1]) * det;
+      G[0 * n2 + q] = s * (Ji[0][0] * Ji[0][0] + Ji[0][1] * Ji[0][1]);
+      G[1 * n2 + q] = s * (Ji[0][0] * Ji[1][0] + Ji[0][1] * Ji[1][1]);
+      G[2 * n2 + q] = s * (Ji[1][0] * Ji[1][0] + Ji[1][1] * Ji[1][1]);
+      if (dJ) dJ[q] = det;
+    }
+  return mind;
+}
+
+// Direct quadrature (O2): v_l = sum_q grad phi_l(q)^T G_q sum_m u_m grad phi_m(q).
+void element_apply2(const Level2& L, const double* G, const double* u, double* v) {
+  const int n = L.n; const int64_t n2 = L.n2;
+  for (int64_t l = 0; l < n2; ++l) v[l] = 0.0;
+  for (int j = 0; j < n; ++j)
+    for (int i = 0; i < n; ++i) {
+      const int q = i + n * j;
+      double g[2] = {0, 0};
+      for (int b = 0; b < n; ++b)
+        for (int a = 0; a < n; ++a) {
+          double d[2];
+          grad_phi2(L.B, i, j, a, b, d);
+          g[0] += d[0] * u[a + n * b]; g[1] += d[1] * u[a + n * b];
+        }
+      const double w0 = G[q] * g[0] + G[n2 + q] * g[1], w1 = G[n2 + q] * g[0] + G[2 * n2 + q] * g[1];
+      for (int b = 0; b < n; ++b)
+        for (int a = 0; a < n; ++a) {
+          double d[2];
+          grad_phi2(L.B, i, j, a, b, d);
+          v[a + n * b] += d[0] * w0 + d[1] * w1;
+        }
+    }
+}
+
+// Dense element matrix K[l][m] = sum_q grad phi_l(q)^T G_q grad phi_m(q).
+void element_matrix2(const Level2& L, const double* G, double* K) {
+  const int n = L.n; const int64_t n2 = L.n2;
+  for (int64_t l = 0; l < n2; ++l)
+    for (int64_t m = 0; m < n2; ++m) {
+      double s = 0.0;
+      for (int j = 0; j < n; ++j)
+        for (int i = 0; i < n; ++i) {
+          const int q = i + n * j;
+          double dl[2], dm[2];
+          grad_phi2(L.B, i, j, (int)(l % n), (int)(l / n), dl);
+          grad_phi2(L.B, i, j, (int)(m % n), (int)(m / n), dm);
+          s += dl[0] * (G[q] * dm[0] + G[n2 + q] * dm[1]) + dl[1] * (G[n2 + q] * dm[0] + G[2 * n2 + q] * dm[1]);
+        }
+      K[l * n2 + m] = s;
+    }
+}
+
+void element_diag2(const Level2& L, const double* G, double* d) {
+  const int n = L.n; const int64_t n2 = L.n2;
+  for (int64_t l = 0; l < n2; ++l) {
+    double s = 0.0;
+    for (int j = 0; j < n; ++j)
+      for (int i = 0; i < n; ++i) {
+        const int q = i + n * j;
+        double dl[2];
+        grad_phi2(L.B, i, j, (int)(l % n), (int)(l / n), dl);
+        s += dl[0] * (G[q] * dl[0] + G[n2 + q] * dl[1]) + dl[1] * (G[n2 + q] * dl[0] + G[2 * n2 + q] * dl[1]);
+      }
+    d[l] = s;
+  }
+}
+
+// A_D u = M A M u + (I - M) u (bc 0, R4); A u (bc 1).
+void apply(const Level2& L, int bc, const double* u, double* v, int) {
+  const int n = L.n; const int64_t n2 = L.n2;
+  std::vector<double> um(u, u + L.N);
+  if (bc == 0)
+    for (int64_t g = 0; g < L.N; ++g) if (L.boundary(g)) um[g] = 0.0;
+  for (int64_t g = 0; g < L.N; ++g) v[g] = 0.0;
+  for (int col = 0; col < 4; ++col) {
+    const std::vector<int64_t>& els = L.colour_elems[col];
+#pragma omp parallel
+    {
+      std::vector<double> ue(n2), ve(n2);
+#pragma omp for schedule(static)
+      for (int64_t t = 0; t < (int64_t)els.size(); ++t) {
+        const int64_t e = els[t];
+        for (int b = 0; b < n; ++b) for (int a = 0; a < n; ++a) ue[a + n * b] = um[L.l2g(e, a, b)];
+        element_apply2(L, &L.G[(size_t)e * 3 * n2], ue.data(), ve.data());
+        for (int b = 0; b < n; ++b) for (int a = 0; a < n; ++a) v[L.l2g(e, a, b)] += ve[a + n * b];
+      }
+    }
+  }
+  if (bc == 0)
+    for (int64_t g = 0; g < L.N; ++g) if (L.boundary(g)) v[g] = u[g];
+}
+
+void compute_diag(const Level2& L, int bc, double* d) {
+  const int n = L.n; const int64_t n2 = L.n2;
+  for (int64_t g = 0; g < L.N; ++g) d[g] = 0.0;
+  std::vector<double> de(n2);
+  for (int64_t e = 0; e < L.E; ++e) {
+    element_diag2(L, &L.G[(size_t)e * 3 * n2], de.data());
+    for (int b = 0; b < n; ++b) for (int a = 0; a < n; ++a) d[L.l2g(e, a, b)] += de[a + n * b];
+  }
+  if (bc == 0)
+    for (int64_t g = 0; g < L.N; ++g) if (L.boundary(g)) d[g] = 1.0;
+}
+
+const std::vector<double>& level_diag(Level2& L) {
+  if (L.diag_cache.empty()) {
+    L.diag_cache.resize(L.N);
+    compute_diag(L, 0, L.diag_cache.data());
+  }
+  return L.diag_cache;
+}
+
+// p-transfer (eq. (7)): P_gJ = phi^C_J(xi(g)) in the canonical element of fine node g; P0 = M_f P M_c.
+void prolong(const Level2& C, const Level2& F, const double* uc, double* uf) {
+  const int nc = C.n;
+  for (int64_t g = 0; g < F.N; ++g) {
+    if (F.boundary(g)) { uf[g] = 0.0; continue; }
+    int ex, ey, i, j;
+    owner_1d(g % F.Mx, F.p, ex, i); owner_1d(g / F.Mx, F.p, ey, j);
+    const int64_t e = ex + (int64_t)C.nex * ey;
+    double s = 0.0;
+    for (int b = 0; b < nc; ++b) for (int a = 0; a < nc; ++a) {
+      const int64_t gc = C.l2g(e, a, b);
+      if (!C.boundary(gc)) s += lagrange(C.B.x, a, F.B.x[i]) * lagrange(C.B.x, b, F.B.x[j]) * uc[gc];
+    }
+    uf[g] = s;
+  }
+}
+// R = P0^T: each interior fine node adds P_gJ r_g to the interior coarse nodes of its canonical element.
+void restrict_(const Level2& C, const Level2& F, const double* rf, double* rc) {
+  const int nc = C.n;
+  for (int64_t g = 0; g < C.N; ++g) rc[g] = 0.0;
+  for (int64_t g = 0; g < F.N; ++g) {
+    if (F.boundary(g)) continue;
+    int ex, ey, i, j;
+    owner_1d(g % F.Mx, F.p, ex, i); owner_1d(g / F.Mx, F.p, ey, j);
+    const int64_t e = ex + (int64_t)C.nex * ey;
+    for (int b = 0; b < nc; ++b) for (int a = 0; a < nc; ++a) {
+      const int64_t gc = C.l2g(e, a, b);
+      if (!C.boundary(gc)) rc[gc] += lagrange(C.B.x, a, F.B.x[i]) * lagrange(C.B.x, b, F.B.x[j]) * rf[g];
+    }
+  }
+}
+// h-transfer (eq. (7) across nested meshes, R25): the coarse basis at the fine node's reference position.
+void prolong_h(const Level2& C, const Level2& F, const double* uc, double* uf) {
+  const int nc = C.n;
+  for (int64_t g = 0; g < F.N; ++g) {
+    if (F.boundary(g)) { uf[g] = 0.0; continue; }
+    int ex, ey; double xi, eta;
+    h_position(g % F.Mx, F.p, F.B.x, F.nex, C.nex, ex, xi);
+    h_position(g / F.Mx, F.p, F.B.x, F.ney, C.ney, ey, eta);
+    const int64_t e = ex + (int64_t)C.nex * ey;
+    double s = 0.0;
+    for (int b = 0; b < nc; ++b) for (int a = 0; a < nc; ++a) {
+      const int64_t gc = C.l2g(e, a, b);
+      if (!C.boundary(gc)) s += lagrange(C.B.x, a, xi) * lagrange(C.B.x, b, eta) * uc[gc];
+    }
+    uf[g] = s;
+  }
+}
+void restrict_h(const Level2& C, const Level2& F, const double* rf, double* rc) {
+  const int nc = C.n;
+  for (int64_t g = 0; g < C.N; ++g) rc[g] = 0.0;
+  for (int64_t g = 0; g < F.N; ++g) {
+    if (F.boundary(g)) continue;
+    int ex, ey; double xi, eta;
+    h_position(g % F.Mx, F.p, F.B.x, F.nex, C.nex, ex, xi);
+    h_position(g / F.Mx, F.p, F.B.x, F.ney, C.ney, ey, eta);
+    const int64_t e = ex + (int64_t)C.nex * ey;
+    for (int b = 0; b < nc; ++b) for (int a = 0; a < nc; ++a) {
+      const int64_t gc = C.l2g(e, a, b);
+      if (!C.boundary(gc)) rc[gc] += lagrange(C.B.x, a, xi) * lagrange(C.B.x, b, eta) * rf[g];
+    }
+  }
+}
+int pair_kind(const Level2& C, const Level2& F) {
+  if (C.nex == F.nex && C.ney == F.ney && F.p == 2 * C.p) return 1;
+  if (C.p == F.p && F.nex == 2 * C.nex && F.ney == 2 * C.ney) return 2;
+  return 0;
+}
+void transfer_prolong(const Level2& C, const Level2& F, const double* uc, double* uf) {
+  if (pair_kind(C, F) == 2) prolong_h(C, F, uc, uf); else prolong(C, F, uc, uf);
+}
+void transfer_restrict(const Level2& C, const Level2& F, const double* rf, double* rc) {
+  if (pair_kind(C, F) == 2) restrict_h(C, F, rf, rc); else restrict_(C, F, rf, rc);
+}
+
+using Hier2 = HierT<Level2>;
+
+// mode 0: MG as solver x <- x + V(b - A x); mode 1: MG-preconditioned CG (Algorithm 1,
+// P:973-991).  x0 = 0 (R14); stop at ||r||_2 <= rtol ||r0||_2.
+// Divergence (||r|| > 10 ||r0||) stops with converged = 0.
+template <class LV>
+int solve_impl(HierT<LV>* H, int mode, const double* b, double* x, double rtol, int maxit,
+               int* iters_out, int* converged, double* r0n, double* rn, double* hist, int hist_cap,
+               int64_t* fine_applies) {
+  LV& L = *H->lv[0];
+  int64_t N = L.N;
+  H->fine_applies = 0;
+  std::vector<double> r(b, b + N), z(N), pv(N), hv(N);
+  for (int64_t g = 0; g < N; ++g) x[g] = 0.0;
+  double r0 = nrm2(r), rnorm = r0;
+  int it = 0, st = 0;
+  *converged = 0;
+  if (hist && hist_cap > 0) hist[0] = r0;
+  if (r0 == 0.0) { *converged = 1; goto done; }
+  if (mode == 0) {
+    while (it < maxit) {
+      if (rnorm <= rtol * r0) { *converged = 1; break; }
+      if (rnorm > 10.0 * r0) break;
+      st = vcycle(*H, 0, r.data(), z.data());
+      if (st) break;
+      for (int64_t g = 0; g < N; ++g) x[g] += z[g];
+      apply(L, 0, x, hv.data(), L.tier);
+      ++H->fine_applies;
+      for (int64_t g = 0; g < N; ++g) r[g] = b[g] - hv[g];
+      rnorm = nrm2(r);
+      ++it;
+      if (hist && it < hist_cap) hist[it] = rnorm;
+    }
+    if (rnorm <= rtol * r0) *converged = 1;
+  } else {
+    st = vcycle(*H, 0, r.data(), z.data());
+    if (st) goto done;
+    pv = z;
+    double rho_r = dot(z, r);
+    while (it < maxit) {
+      apply(L, 0, pv.data(), hv.data(), L.tier);                 // h = A p
+      ++H->fine_applies;
+      double ph = dot(pv, hv);
+      if (ph <= 0.0) { st = 6; break; }
+      double alpha = rho_r / ph;
+      for (int64_t g = 0; g < N; ++g) { x[g] += alpha * pv[g]; r[g] -= alpha * hv[g]; }
+      rnorm = nrm2(r);
+      ++it;
+      if (hist && it < hist_cap) hist[it] = rnorm;
+      if (rnorm <= rtol * r0) { *converged = 1; break; }      // convergence test
+      if (rnorm > 10.0 * r0) break;
+      st = vcycle(*H, 0, r.data(), z.data());                  // rho = M r
+      if (st) break;
+      double rho_new = dot(z, r);
+      double beta = rho_new / rho_r;
+      for (int64_t g = 0; g < N; ++g) pv[g] = z[g] + beta * pv[g];
+      rho_r = rho_new;
+    }
+  }
+done:
+  *iters_out = it;
+  *r0n = r0; *rn = rnorm;
+  *fine_applies = H->fine_applies;
+  return st;
 }
 
 }  // namespace
@@ -1387,62 +1751,177 @@ int orc_vcycle(void* h, const double* b, double* x) {
 int orc_solve(void* h, int mode, const double* b, double* x, double rtol, int maxit,
               int* iters_out, int* converged, double* r0n, double* rn, double* hist, int hist_cap,
               int64_t* fine_applies) {
-  Hier* H = (Hier*)h;
-  Level& L = *H->lv[0];
-  int64_t N = L.N;
-  H->fine_applies = 0;
-  std::vector<double> r(b, b + N), z(N), pv(N), hv(N);
-  for (int64_t g = 0; g < N; ++g) x[g] = 0.0;
-  double r0 = nrm2(r), rnorm = r0;
-  int it = 0, st = 0;
-  *converged = 0;
-  if (hist && hist_cap > 0) hist[0] = r0;
-  if (r0 == 0.0) { *converged = 1; goto done; }
-  if (mode == 0) {
-    while (it < maxit) {
-      if (rnorm <= rtol * r0) { *converged = 1; break; }
-      if (rnorm > 10.0 * r0) break;
-      st = vcycle(*H, 0, r.data(), z.data());
-      if (st) break;
-      for (int64_t g = 0; g < N; ++g) x[g] += z[g];
-      apply(L, 0, x, hv.data(), L.tier);
-      ++H->fine_applies;
-      for (int64_t g = 0; g < N; ++g) r[g] = b[g] - hv[g];
-      rnorm = nrm2(r);
-      ++it;
-      if (hist && it < hist_cap) hist[it] = rnorm;
-    }
-    if (rnorm <= rtol * r0) *converged = 1;
-  } else {
-    st = vcycle(*H, 0, r.data(), z.data());
-    if (st) goto done;
-    pv = z;
-    double rho_r = dot(z, r);
-    while (it < maxit) {
-      apply(L, 0, pv.data(), hv.data(), L.tier);                 // h = A p
-      ++H->fine_applies;
-      double ph = dot(pv, hv);
-      if (ph <= 0.0) { st = 6; break; }
-      double alpha = rho_r / ph;
-      for (int64_t g = 0; g < N; ++g) { x[g] += alpha * pv[g]; r[g] -= alpha * hv[g]; }
-      rnorm = nrm2(r);
-      ++it;
-      if (hist && it < hist_cap) hist[it] = rnorm;
-      if (rnorm <= rtol * r0) { *converged = 1; break; }      // convergence test
-      if (rnorm > 10.0 * r0) break;
-      st = vcycle(*H, 0, r.data(), z.data());                  // rho = M r
-      if (st) break;
-      double rho_new = dot(z, r);
-      double beta = rho_new / rho_r;
-      for (int64_t g = 0; g < N; ++g) pv[g] = z[g] + beta * pv[g];
-      rho_r = rho_new;
-    }
+  return solve_impl((Hier*)h, mode, b, x, rtol, maxit, iters_out, converged, r0n, rn, hist, hist_cap, fine_applies);
+}
+
+/* ---------------------------------------------------------------- NEXT-2: 2-D C ABI (orc2_*) */
+void* orc2_level_create(int nex, int ney, int p, int warp, double amp, int coeff, double c0, double c1) {
+  if (p < 1 || p > 16 || nex < 1 || ney < 1) return nullptr;
+  Level2* L = new Level2();
+  L->nex = nex; L->ney = ney; L->p = p; L->n = p + 1;
+  L->warp = warp; L->amp = amp; L->coeff = coeff; L->c0 = c0; L->c1 = c1;
+  L->E = (int64_t)nex * ney;
+  L->Mx = (int64_t)nex * p + 1; L->My = (int64_t)ney * p + 1;
+  L->N = L->Mx * L->My;
+  L->n2 = (int64_t)L->n * L->n;
+  L->B.build(p, g_quad);
+  L->colour_elems.assign(4, {});
+  for (int64_t e = 0; e < L->E; ++e) {
+    int ex, ey; L->elem_coords(e, ex, ey);
+    L->colour_elems[(ex & 1) | ((ey & 1) << 1)].push_back(e);
   }
-done:
-  *iters_out = it;
-  *r0n = r0; *rn = rnorm;
-  *fine_applies = H->fine_applies;
-  return st;
+  L->G.resize((size_t)L->E * 3 * L->n2);
+  L->detJ.resize((size_t)L->E * L->n2);
+  double mind = 1e300;
+  for (int64_t e = 0; e < L->E; ++e)
+    mind = std::min(mind, element_geometry2(*L, e, &L->G[(size_t)e * 3 * L->n2], &L->detJ[(size_t)e * L->n2]));
+  L->min_detj = mind;
+  if (!(mind > 0.0)) L->status = 4;
+  return L;
+}
+void orc2_level_destroy(void* h) { delete (Level2*)h; }
+int orc2_level_status(void* h) { return ((Level2*)h)->status; }
+int64_t orc2_level_ndofs(void* h) { return ((Level2*)h)->N; }
+int orc2_mask(void* h, uint8_t* mask) {
+  Level2* L = (Level2*)h;
+  for (int64_t g = 0; g < L->N; ++g) mask[g] = L->boundary(g) ? 1 : 0;
+  return 0;
+}
+int orc2_geometry(void* h, int64_t e, double* G) {
+  Level2* L = (Level2*)h;
+  for (int64_t i = 0; i < 3 * L->n2; ++i) G[i] = L->G[(size_t)e * 3 * L->n2 + i];
+  return 0;
+}
+int orc2_element_matrix(void* h, int64_t e, double* K) {
+  Level2* L = (Level2*)h;
+  element_matrix2(*L, &L->G[(size_t)e * 3 * L->n2], K);
+  return 0;
+}
+// Dense A_D (bc 0) or A (bc 1) assembled from the element matrices (O1), small meshes only.
+int orc2_assemble_dense(void* h, int bc, double* A) {
+  Level2* L = (Level2*)h;
+  const int n = L->n; const int64_t n2 = L->n2, N = L->N;
+  for (int64_t i = 0; i < N * N; ++i) A[i] = 0.0;
+  std::vector<double> K(n2 * n2);
+  for (int64_t e = 0; e < L->E; ++e) {
+    element_matrix2(*L, &L->G[(size_t)e * 3 * n2], K.data());
+    for (int64_t l = 0; l < n2; ++l)
+      for (int64_t m = 0; m < n2; ++m) A[L->l2g(e, (int)(l % n), (int)(l / n)) * N + L->l2g(e, (int)(m % n), (int)(m / n))] += K[l * n2 + m];
+  }
+  if (bc == 0)
+    for (int64_t g = 0; g < N; ++g)
+      if (L->boundary(g)) {
+        for (int64_t k = 0; k < N; ++k) { A[g * N + k] = 0.0; A[k * N + g] = 0.0; }
+        A[g * N + g] = 1.0;
+      }
+  return 0;
+}
+int orc2_apply(void* h, int bc, const double* u, double* v) { apply(*(Level2*)h, bc, u, v, 2); return 0; }
+int orc2_diag(void* h, int bc, double* d) { compute_diag(*(Level2*)h, bc, d); return 0; }
+double orc2_lambda_max(void* h, int iters, uint64_t seed) { return lambda_max(*(Level2*)h, iters, seed, nullptr); }
+double orc2_lambda_arnoldi(void* h, int m, uint64_t seed) { return lambda_arnoldi(*(Level2*)h, m, seed, nullptr); }
+int orc2_cheb(void* h, const double* b, double* x, int K, double lo, double hi) {
+  chebyshev(*(Level2*)h, b, x, K, lo, hi, nullptr);
+  return 0;
+}
+int orc2_jacobi(void* h, const double* b, double* x, int steps, double omega) {
+  jacobi(*(Level2*)h, b, x, steps, omega, nullptr);
+  return 0;
+}
+int orc2_prolong(void* hc, void* hf, const double* uc, double* uf) {
+  Level2 *C = (Level2*)hc, *F = (Level2*)hf;
+  if (!pair_kind(*C, *F)) return 5;
+  transfer_prolong(*C, *F, uc, uf);
+  return 0;
+}
+int orc2_restrict(void* hc, void* hf, const double* rf, double* rc) {
+  Level2 *C = (Level2*)hc, *F = (Level2*)hf;
+  if (!pair_kind(*C, *F)) return 5;
+  transfer_restrict(*C, *F, rf, rc);
+  return 0;
+}
+// Manufactured solution u* = sin(pi x) sin(pi y): f = -div(mu grad u*) = 2 pi^2 mu u* - grad mu . grad u*,
+// b_l = (1 - bnd) sum_{e, q} phi_l(x_q) w_q detJ_q f(x_q); rhs_id 1.
+int orc2_load_vector(void* h, int rhs_id, double* f) {
+  Level2* L = (Level2*)h;
+  if (rhs_id != 1) return 1;
+  const int n = L->n; const int64_t n2 = L->n2;
+  for (int64_t g = 0; g < L->N; ++g) f[g] = 0.0;
+  std::vector<double> X;
+  for (int64_t e = 0; e < L->E; ++e) {
+    element_nodes2(*L, e, X);
+    for (int j = 0; j < n; ++j)
+      for (int i = 0; i < n; ++i) {
+        double x = 0.0, y = 0.0;
+        for (int b = 0; b < n; ++b) for (int a = 0; a < n; ++a) {
+          const double ph = L->B.L[i * n + a] * L->B.L[j * n + b];
+          x += ph * X[a + n * b]; y += ph * X[n2 + a + n * b];
+        }
+        const double us = std::sin(kPi * x) * std::sin(kPi * y);
+        const double gu[2] = {kPi * std::cos(kPi * x) * std::sin(kPi * y), kPi * std::sin(kPi * x) * std::cos(kPi * y)};
+        double gm[2];
+        coeff_grad2(L->coeff, L->c0, L->c1, x, y, gm);
+        const double fx = 2.0 * kPi * kPi * coeff_mu2(L->coeff, L->c0, L->c1, x, y) * us - (gm[0] * gu[0] + gm[1] * gu[1]);
+        const double wq = L->B.qw[i] * L->B.qw[j] * L->detJ[(size_t)e * n2 + i + n * j] * fx;
+        for (int b = 0; b < n; ++b) for (int a = 0; a < n; ++a)
+          f[L->l2g(e, a, b)] += L->B.L[i * n + a] * L->B.L[j * n + b] * wq;
+      }
+  }
+  for (int64_t g = 0; g < L->N; ++g) if (L->boundary(g)) f[g] = 0.0;
+  return 0;
+}
+int orc2_exact_solution(void* h, double* u) {
+  Level2* L = (Level2*)h;
+  const int n = L->n;
+  std::vector<double> X;
+  for (int64_t e = 0; e < L->E; ++e) {
+    element_nodes2(*L, e, X);
+    for (int b = 0; b < n; ++b) for (int a = 0; a < n; ++a)
+      u[L->l2g(e, a, b)] = std::sin(kPi * X[a + n * b]) * std::sin(kPi * X[L->n2 + a + n * b]);
+  }
+  return 0;
+}
+// Hierarchy (as orc_hier_create3): coarsen 0: p, p/2, ..., 1 then h_levels meshes at p = 1;
+// coarsen 1: order p on ne, ne/2, ..., ne/2^h_levels ("32x32, 16x16 and 8x8").
+void* orc2_hier_create(int nex, int ney, int p, int warp, double amp, int coeff, double c0, double c1, int nu_pre,
+                       int nu_post, int K, double lo_frac, double hi_frac, int power_iters, uint64_t seed,
+                       double coarse_rtol, int coarse_maxit, int smoother, double omega, int lambda_method,
+                       int h_levels, int coarsen, int* status) {
+  *status = 0;
+  const int pmin = (coarsen == 1) ? p : 1;
+  for (int q = p; q > pmin; q /= 2)
+    if (q % 2) { *status = 5; return nullptr; }
+  for (int j = 0; j < h_levels; ++j)
+    if (((nex >> j) % 2) || ((ney >> j) % 2)) { *status = 5; return nullptr; }
+  Hier2* H = new Hier2();
+  H->nu_pre = nu_pre; H->nu_post = nu_post; H->K = K; H->lo_frac = lo_frac; H->hi_frac = hi_frac;
+  H->power_iters = power_iters; H->seed = seed; H->coarse_rtol = coarse_rtol; H->coarse_maxit = coarse_maxit;
+  H->smoother = smoother; H->omega = omega; H->lambda_method = lambda_method;
+  for (int q = p; q >= pmin; q /= 2) {
+    H->lv.push_back((Level2*)orc2_level_create(nex, ney, q, warp, amp, coeff, c0, c1));
+    if (q == pmin) break;
+  }
+  for (int j = 1; j <= h_levels; ++j)
+    H->lv.push_back((Level2*)orc2_level_create(nex >> j, ney >> j, pmin, warp, amp, coeff, c0, c1));
+  for (Level2* L : H->lv) if (L->status) *status = L->status;
+  H->lam.assign(H->lv.size(), 0.0);
+  for (size_t l = 0; l + 1 < H->lv.size(); ++l)
+    H->lam[l] = lambda_method == 1 ? lambda_arnoldi(*H->lv[l], power_iters, seed, nullptr)
+                                   : lambda_max(*H->lv[l], power_iters, seed, nullptr);
+  return H;
+}
+void orc2_hier_destroy(void* h) {
+  Hier2* H = (Hier2*)h;
+  for (Level2* L : H->lv) delete L;
+  delete H;
+}
+int orc2_hier_nlevels(void* h) { return (int)((Hier2*)h)->lv.size(); }
+void* orc2_hier_level(void* h, int l) { return ((Hier2*)h)->lv[l]; }
+double orc2_hier_lambda(void* h, int l) { return ((Hier2*)h)->lam[l]; }
+int orc2_vcycle(void* h, const double* b, double* x) { return vcycle(*(Hier2*)h, 0, b, x); }
+int orc2_solve(void* h, int mode, const double* b, double* x, double rtol, int maxit, int* iters_out, int* converged,
+               double* r0n, double* rn, double* hist, int hist_cap, int64_t* fine_applies) {
+  return solve_impl((Hier2*)h, mode, b, x, rtol, maxit, iters_out, converged, r0n, rn, hist, hist_cap, fine_applies);
 }
 
 }  // extern "C"
