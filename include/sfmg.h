@@ -62,6 +62,13 @@ typedef struct {
                            /* 1: (p+1)^3 Gauss-Legendre points, nodal LGL basis ("Gauss   */
                            /*    quadrature"): G is stored at the Gauss     */
                            /*    points and the apply adds interpolation passes               */
+  int32_t dim;             /* 0 or 3: hexahedra (above); 2: quadrilaterals on [0,1]^2 (SURVEY 8(f)  */
+                           /*    NEXT-2): nex x ney elements (nez must be 0 or 1),     */
+                           /*    warp x_i += warp_amp sin(pi x) sin(pi y), mu kinds 0-2 with       */
+                           /*    S = sin2pix sin2piy, 3: c0 + c1 (cos^2 2pi x + cos^2 2pi y)       */
+                           /*    (2d-var), 4: c0 + c1 (cos^2 10pi x + cos^2 10pi y) (2d-var');    */
+                           /*    every call below applies with (p+1)^2 per element.  Not for 2-D: */
+                           /*    sfmg_export_l2g / _mask / _colors / _geometry (SFMG_E_ARG).      */
 } sfmg_problem;
 
 /* p-multigrid parameters (R7-R11, R13).  The last four fields select

@@ -12,7 +12,7 @@ CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 BUILD = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "libsfmg.so")
-SOURCES = ["basis.cu", "k_operator.cu", "k_gauss.cu", "k_blas.cu", "k_transfer.cu", "sfmg_api.cu"]
+SOURCES = ["basis.cu", "k_operator.cu", "k_gauss.cu", "k_2d.cu", "k_blas.cu", "k_transfer.cu", "sfmg_api.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",

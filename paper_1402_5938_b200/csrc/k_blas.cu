@@ -8,13 +8,13 @@ namespace sfmg {
 
 constexpr int kRedThreads = 256;
 
-__device__ __forceinline__ bool vec_boundary(int Mx, int My, int Mz, long long g) {
+__device__ __forceinline__ bool vec_boundary(int Mx, int My, int Kb0, int Kb1, long long g) {
   unsigned int gi = (unsigned int)g;
   unsigned int I = gi % (unsigned)Mx;
   unsigned int r = gi / (unsigned)Mx;
   unsigned int J = r % (unsigned)My;
   unsigned int K = r / (unsigned)My;
-  return I == 0 || I == (unsigned)Mx - 1 || J == 0 || J == (unsigned)My - 1 || K == 0 || K == (unsigned)Mz - 1;
+  return I == 0 || I == (unsigned)Mx - 1 || J == 0 || J == (unsigned)My - 1 || (int)K == Kb0 || (int)K == Kb1;
 }
 
 // Block-level sum of NV values per thread into partials[blockIdx][slot..]; returns true in the
@@ -92,13 +92,13 @@ __global__ void __launch_bounds__(kRedThreads) k_power_sums(RedScratch r, const 
   }
 }
 
-__global__ void k_power_norm(int Mx, int My, int Mz, const double* __restrict__ scal, double* x, double* y,
+__global__ void k_power_norm(int Mx, int My, int Kb0, int Kb1, const double* __restrict__ scal, double* x, double* y,
                              const double* __restrict__ dinv, long long n) {
   const double s = scal[4];
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     const double xn = y[i] * dinv[i] * s;
     x[i] = xn;
-    y[i] = vec_boundary(Mx, My, Mz, i) ? xn : 0.0;
+    y[i] = vec_boundary(Mx, My, Kb0, Kb1, i) ? xn : 0.0;
   }
 }
 
@@ -111,9 +111,9 @@ __device__ __forceinline__ double uniform_pm1(unsigned long long seed, unsigned 
   return 2.0 * ((double)(z >> 11) * (1.0 / 9007199254740992.0)) - 1.0;
 }
 
-__global__ void k_power_start(int Mx, int My, int Mz, unsigned long long seed, double* x, double* y, long long n) {
+__global__ void k_power_start(int Mx, int My, int Kb0, int Kb1, unsigned long long seed, double* x, double* y, long long n) {
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    const bool b = vec_boundary(Mx, My, Mz, i);
+    const bool b = vec_boundary(Mx, My, Kb0, Kb1, i);
     x[i] = b ? 0.0 : uniform_pm1(seed, (unsigned long long)i);
     y[i] = 0.0;
   }
@@ -243,11 +243,11 @@ cudaError_t launch_dot(const RedScratch& r, const double* a, const double* b, lo
 cudaError_t launch_power_step(const MeshDev& m, const RedScratch& r, double* x, double* y, const double* dinv,
                               cudaStream_t s) {
   k_power_sums<<<kRedBlocks, kRedThreads, 0, s>>>(r, x, y, dinv, m.N);
-  k_power_norm<<<vgrid(m.N), 256, 0, s>>>(m.Mx, m.My, m.Mz, r.scalars, x, y, dinv, m.N);
+  k_power_norm<<<vgrid(m.N), 256, 0, s>>>(m.Mx, m.My, m.Kb0, m.Kb1, r.scalars, x, y, dinv, m.N);
   return cudaGetLastError();
 }
 cudaError_t launch_power_start(const MeshDev& m, uint64_t seed, double* x, double* y, cudaStream_t s) {
-  k_power_start<<<vgrid(m.N), 256, 0, s>>>(m.Mx, m.My, m.Mz, (unsigned long long)seed, x, y, m.N);
+  k_power_start<<<vgrid(m.N), 256, 0, s>>>(m.Mx, m.My, m.Kb0, m.Kb1, (unsigned long long)seed, x, y, m.N);
   return cudaGetLastError();
 }
 cudaError_t launch_pcg_xr(const RedScratch& red, double* x, double* r, const double* p, const double* h, int ia,

@@ -42,8 +42,8 @@ __device__ __forceinline__ bool lattice_boundary(const MeshDev& m, long long g) 
   unsigned int r = gi / (unsigned)m.Mx;
   unsigned int J = r % (unsigned)m.My;
   unsigned int K = r / (unsigned)m.My;
-  return I == 0 || I == (unsigned)m.Mx - 1 || J == 0 || J == (unsigned)m.My - 1 || K == 0 ||
-         K == (unsigned)m.Mz - 1;
+  return I == 0 || I == (unsigned)m.Mx - 1 || J == 0 || J == (unsigned)m.My - 1 || (int)K == m.Kb0 ||
+         (int)K == m.Kb1;   // z planes: 0 and Mz - 1 in 3-D, none in 2-D
 }
 
 // mu at a physical point (R3, R6)

@@ -94,6 +94,30 @@ static double lag_der(const std::vector<double>& xs, int a, double t) {
   return s;
 }
 
+// 1-D tables of one order for the 2-D kernels (k_2d.cu): LGL nodes, and the basis / derivative at the
+// quadrature points with their weights: quad 0 collocated LGL (B = I, DB = D, w_LGL), quad 1 Gauss.
+void quad_tables_1d(int p, int quad, std::vector<double>& xn, std::vector<double>& B, std::vector<double>& DB,
+                    std::vector<double>& qw) {
+  const int n = p + 1;
+  Basis1D L = make_basis(p);
+  xn = L.x;
+  B.assign(n * n, 0.0);
+  DB.assign(n * n, 0.0);
+  if (quad == 0) {
+    for (int i = 0; i < n; ++i) B[i * n + i] = 1.0;
+    DB = L.D;
+    qw = L.w;
+    return;
+  }
+  std::vector<double> gx;
+  gauss_rule(n, gx, qw);
+  for (int i = 0; i < n; ++i)
+    for (int a = 0; a < n; ++a) {
+      B[i * n + a] = lag_val(L.x, a, gx[i]);
+      DB[i * n + a] = lag_der(L.x, a, gx[i]);
+    }
+}
+
 static bool g_gauss_uploaded[kMaxOrder + 1];
 
 cudaError_t upload_gauss_tables(int p) {

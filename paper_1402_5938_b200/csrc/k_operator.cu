@@ -1026,6 +1026,7 @@ static void geometry_p(const MeshDev& m, double* G, int* bad, cudaStream_t s) {
   k_geometry<P><<<grid_for(m.E * N3, 256), 256, 0, s>>>(m, G, bad);
 }
 cudaError_t launch_geometry(const MeshDev& m, double* G, int* bad, cudaStream_t s) {
+  if (m.dim == 2) return launch_geometry_2d(m, G, bad, s);
   if (m.quad) return launch_geometry_gauss(m, G, bad, s);
   SFMG_DISPATCH_P(m.p, geometry_p, m, G, bad, s);
   return cudaGetLastError();
@@ -1093,6 +1094,7 @@ static void apply_p(const MeshDev& m, int bc, const double* G, const double* u, 
 }
 cudaError_t launch_apply(const MeshDev& m, int bc, const double* G, const double* u, double* v, int wait_mode,
                          int write_bnd, cudaStream_t s) {
+  if (m.dim == 2) return launch_apply_2d(m, bc, G, u, v, s);   // v initialised by the caller (no PDL)
   if (m.quad) return launch_apply_gauss(m, bc, G, u, v, s);   // v initialised by the caller (no PDL)
   cudaError_t err = cudaSuccess;
   SFMG_DISPATCH_P(m.p, apply_p, m, bc, G, u, v, wait_mode, write_bnd, s, &err);
@@ -1108,6 +1110,7 @@ static void diag_p(const MeshDev& m, int bc, const double* G, double* d, cudaStr
 cudaError_t launch_diag(const MeshDev& m, int bc, const double* G, double* d, cudaStream_t s) {
   cudaError_t e = launch_init(m, bc, nullptr, 1.0, d, s);
   if (e) return e;
+  if (m.dim == 2) return launch_diag_2d(m, bc, G, d, s);
   if (m.quad) return launch_diag_gauss(m, bc, G, d, s);
   SFMG_DISPATCH_P(m.p, diag_p, m, bc, G, d, s);
   return cudaGetLastError();
@@ -1122,6 +1125,7 @@ cudaError_t launch_load(const MeshDev& m, int rhs_id, double* f, cudaStream_t s)
   if (rhs_id != 1) return cudaErrorInvalidValue;
   cudaError_t e = launch_init(m, 1, nullptr, 0.0, f, s);
   if (e) return e;
+  if (m.dim == 2) return launch_load_2d(m, f, s);
   if (m.quad) return launch_load_gauss(m, f, s);
   SFMG_DISPATCH_P(m.p, load_p, m, f, s);
   return cudaGetLastError();

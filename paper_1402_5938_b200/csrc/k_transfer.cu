@@ -493,4 +493,148 @@ cudaError_t launch_restrict_hp(const MeshDev& mc, const MeshDev& mf, const doubl
   SFMG_HP_CASES(restrict_hp_p, mc, mf, rf, rc, s)
 }
 
+// ------------------------------------------------------------------------------------------
+// 2-D transfers (NEXT-2): the same eq. (7) contractions on quadrilaterals, block per fine element.
+// KIND 1: p pair (fine order 2 PC, same element grid, matrix c_I); KIND 2: h pair at order PC (fine
+// element (ex, ey) is child (ex & 1, ey & 1) of coarse element (ex/2, ey/2), matrices c_H).
+
+template <int PC, int KIND>
+struct X2 {
+  static constexpr int PF = KIND == 1 ? 2 * PC : PC, NC = PC + 1, NF = PF + 1;
+  __device__ static double M(int s, int i, int a) {   // fine index i, coarse index a
+    if constexpr (KIND == 1) return c_I[PC - 1][i * NC + a];
+    else return hmat<PC>(s, i, a);
+  }
+};
+
+template <int PC, int KIND>
+__global__ void __launch_bounds__(128) k_prolong2d(MeshDev mc, MeshDev mf, const double* __restrict__ uc,
+                                                   double* __restrict__ uf, int add) {
+  using X = X2<PC, KIND>;
+  constexpr int NC = X::NC, NF = X::NF, PF = X::PF;
+  __shared__ double sc[NC * NC], t1[NF * NC];
+  for (long long e = blockIdx.x; e < mf.E; e += gridDim.x) {
+    const int ex = (int)(e % mf.nex), ey = (int)(e / mf.nex);
+    const int cx = KIND == 1 ? ex : ex >> 1, cy = KIND == 1 ? ey : ey >> 1;
+    const int sx = ex & 1, sy = ey & 1;
+    __syncthreads();
+    for (int l = threadIdx.x; l < NC * NC; l += blockDim.x) {
+      const int a = l % NC, b = l / NC, I = cx * PC + a, J = cy * PC + b;
+      const bool bnd = I == 0 || I == mc.Mx - 1 || J == 0 || J == mc.My - 1;
+      sc[l] = bnd ? 0.0 : uc[I + (long long)mc.Mx * J];
+    }
+    __syncthreads();
+    for (int l = threadIdx.x; l < NF * NC; l += blockDim.x) {
+      const int i = l % NF, b = l / NF;
+      double s = 0.0;
+#pragma unroll
+      for (int a = 0; a < NC; ++a) s += X::M(sx, i, a) * sc[a + NC * b];
+      t1[l] = s;
+    }
+    __syncthreads();
+    for (int l = threadIdx.x; l < NF * NF; l += blockDim.x) {
+      const int i = l % NF, j = l / NF;
+      if ((i == 0 && ex > 0) || (j == 0 && ey > 0)) continue;   // not the owner
+      const int I = ex * PF + i, J = ey * PF + j;
+      const long long g = I + (long long)mf.Mx * J;
+      if (I == 0 || I == mf.Mx - 1 || J == 0 || J == mf.My - 1) {
+        if (!add) uf[g] = 0.0;
+        continue;
+      }
+      double s = 0.0;
+#pragma unroll
+      for (int b = 0; b < NC; ++b) s += X::M(sy, j, b) * t1[i + NF * b];
+      if (add) uf[g] += s; else uf[g] = s;
+    }
+  }
+}
+
+template <int PC, int KIND>
+__global__ void __launch_bounds__(128) k_restrict2d(MeshDev mc, MeshDev mf, const double* __restrict__ rf,
+                                                    double* __restrict__ rc) {
+  using X = X2<PC, KIND>;
+  constexpr int NC = X::NC, NF = X::NF, PF = X::PF;
+  __shared__ double sf[NF * NF], t1[NC * NF];
+  for (long long e = blockIdx.x; e < mf.E; e += gridDim.x) {
+    const int ex = (int)(e % mf.nex), ey = (int)(e / mf.nex);
+    const int cx = KIND == 1 ? ex : ex >> 1, cy = KIND == 1 ? ey : ey >> 1;
+    const int sx = ex & 1, sy = ey & 1;
+    __syncthreads();
+    for (int l = threadIdx.x; l < NF * NF; l += blockDim.x) {
+      const int i = l % NF, j = l / NF, I = ex * PF + i, J = ey * PF + j;
+      const bool own = !((i == 0 && ex > 0) || (j == 0 && ey > 0));
+      const bool bnd = I == 0 || I == mf.Mx - 1 || J == 0 || J == mf.My - 1;
+      sf[l] = (own && !bnd) ? rf[I + (long long)mf.Mx * J] : 0.0;
+    }
+    __syncthreads();
+    for (int l = threadIdx.x; l < NC * NF; l += blockDim.x) {
+      const int a = l % NC, j = l / NC;
+      double s = 0.0;
+#pragma unroll
+      for (int i = 0; i < NF; ++i) s += X::M(sx, i, a) * sf[i + NF * j];
+      t1[l] = s;
+    }
+    __syncthreads();
+    for (int l = threadIdx.x; l < NC * NC; l += blockDim.x) {
+      const int a = l % NC, b = l / NC, I = cx * PC + a, J = cy * PC + b;
+      if (I == 0 || I == mc.Mx - 1 || J == 0 || J == mc.My - 1) continue;
+      double s = 0.0;
+#pragma unroll
+      for (int j = 0; j < NF; ++j) s += X::M(sy, j, b) * t1[a + NC * j];
+      atomicAdd(rc + I + (long long)mc.Mx * J, s);
+    }
+  }
+}
+
+static unsigned xgrid2(long long E) {
+  long long b = E;
+  if (b > 148LL * 16) b = 148LL * 16;
+  return (unsigned)(b < 1 ? 1 : b);
+}
+
+template <int PC, int KIND>
+static cudaError_t xfer2d(const MeshDev& mc, const MeshDev& mf, const double* in, double* out, int add, int dir,
+                          cudaStream_t s) {
+  if (dir == 0) {
+    k_prolong2d<PC, KIND><<<xgrid2(mf.E), 128, 0, s>>>(mc, mf, in, out, add);
+  } else {
+    cudaError_t e = cudaMemsetAsync(out, 0, sizeof(double) * mc.N, s);
+    if (e) return e;
+    k_restrict2d<PC, KIND><<<xgrid2(mf.E), 128, 0, s>>>(mc, mf, in, out);
+  }
+  return cudaGetLastError();
+}
+
+// dir 0: out = P0 in (+= if add); dir 1: out = P0^T in.  kind 1 p pair (coarse p <= 8), 2 h pair.
+cudaError_t launch_transfer_2d(const MeshDev& mc, const MeshDev& mf, int kind, int dir, const double* in, double* out,
+                               int add, cudaStream_t s) {
+  cudaError_t e;
+  if (kind == 1) {
+    if ((e = upload_interp_tables(mc.p, s))) return e;
+    switch (mc.p) {
+      case 1: return xfer2d<1, 1>(mc, mf, in, out, add, dir, s);
+      case 2: return xfer2d<2, 1>(mc, mf, in, out, add, dir, s);
+      case 3: return xfer2d<3, 1>(mc, mf, in, out, add, dir, s);
+      case 4: return xfer2d<4, 1>(mc, mf, in, out, add, dir, s);
+      case 5: return xfer2d<5, 1>(mc, mf, in, out, add, dir, s);
+      case 6: return xfer2d<6, 1>(mc, mf, in, out, add, dir, s);
+      case 7: return xfer2d<7, 1>(mc, mf, in, out, add, dir, s);
+      case 8: return xfer2d<8, 1>(mc, mf, in, out, add, dir, s);
+    }
+    return cudaErrorInvalidValue;
+  }
+  if ((e = upload_h_tables(mc.p))) return e;
+  switch (mc.p) {
+    case 1: return xfer2d<1, 2>(mc, mf, in, out, add, dir, s);   case 2: return xfer2d<2, 2>(mc, mf, in, out, add, dir, s);
+    case 3: return xfer2d<3, 2>(mc, mf, in, out, add, dir, s);   case 4: return xfer2d<4, 2>(mc, mf, in, out, add, dir, s);
+    case 5: return xfer2d<5, 2>(mc, mf, in, out, add, dir, s);   case 6: return xfer2d<6, 2>(mc, mf, in, out, add, dir, s);
+    case 7: return xfer2d<7, 2>(mc, mf, in, out, add, dir, s);   case 8: return xfer2d<8, 2>(mc, mf, in, out, add, dir, s);
+    case 9: return xfer2d<9, 2>(mc, mf, in, out, add, dir, s);   case 10: return xfer2d<10, 2>(mc, mf, in, out, add, dir, s);
+    case 11: return xfer2d<11, 2>(mc, mf, in, out, add, dir, s); case 12: return xfer2d<12, 2>(mc, mf, in, out, add, dir, s);
+    case 13: return xfer2d<13, 2>(mc, mf, in, out, add, dir, s); case 14: return xfer2d<14, 2>(mc, mf, in, out, add, dir, s);
+    case 15: return xfer2d<15, 2>(mc, mf, in, out, add, dir, s); case 16: return xfer2d<16, 2>(mc, mf, in, out, add, dir, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
 }  // namespace sfmg

@@ -33,12 +33,15 @@ static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 static sfmg_status check_problem(const sfmg_problem* pr) {
   if (!pr) { set_error("null problem"); return SFMG_E_ARG; }
   if (pr->order < 1 || pr->order > kMaxOrder) { set_error("order must be 1..16"); return SFMG_E_ORDER; }
-  if (pr->nex < 1 || pr->ney < 1 || pr->nez < 1) { set_error("element counts must be >= 1"); return SFMG_E_MESH; }
+  if (pr->dim != 0 && pr->dim != 2 && pr->dim != 3) { set_error("dim must be 0, 2 or 3"); return SFMG_E_ARG; }
+  const bool two = pr->dim == 2;
+  if (two && pr->nez > 1) { set_error("2-D problems have nez = 0 or 1"); return SFMG_E_MESH; }
+  if (pr->nex < 1 || pr->ney < 1 || (!two && pr->nez < 1)) { set_error("element counts must be >= 1"); return SFMG_E_MESH; }
   long long Mx = (long long)pr->nex * pr->order + 1, My = (long long)pr->ney * pr->order + 1,
-            Mz = (long long)pr->nez * pr->order + 1;
+            Mz = two ? 1 : (long long)pr->nez * pr->order + 1;
   if (Mx * My * Mz >= (1LL << 31)) { set_error("lattice exceeds 2^31 nodes"); return SFMG_E_MESH; }
   if (pr->warp != 0 && pr->warp != 1) { set_error("warp must be 0 or 1"); return SFMG_E_ARG; }
-  if (pr->coeff < 0 || pr->coeff > 3) { set_error("coeff must be 0..3"); return SFMG_E_ARG; }
+  if (pr->coeff < 0 || pr->coeff > (two ? 4 : 3)) { set_error("coeff must be 0..3 (2-D: 0..4)"); return SFMG_E_ARG; }
   if (pr->quadrature != 0 && pr->quadrature != 1) { set_error("quadrature must be 0 or 1"); return SFMG_E_ARG; }
   return SFMG_OK;
 }
@@ -53,6 +56,14 @@ static MeshDev make_mesh(const sfmg_problem* pr) {
   m.amp = pr->warp_amp; m.c0 = pr->c0; m.c1 = pr->c1;
   m.quad = pr->quadrature;
   m.Kb0 = 0; m.Kb1 = m.Mz - 1;
+  if (pr->dim == 2) {   // quadrilaterals: one lattice plane, no z boundary (NEXT-2)
+    m.dim = 2;
+    m.nez = 1;
+    m.Mz = 1;
+    m.E = (long long)m.nex * m.ney;
+    m.N = (long long)m.Mx * m.My;
+    m.Kb0 = m.Kb1 = -1;
+  }
   return m;
 }
 
@@ -65,7 +76,8 @@ static LevelLayout level_layout(const MeshDev& m) {
   const long long n3 = (long long)(m.p + 1) * (m.p + 1) * (m.p + 1);
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off += align_up(bytes); return o; };
-  L.G = take(sizeof(double) * 6 * (size_t)geometry_elems(m.p, m.E) * n3);
+  if (m.dim == 2) L.G = take(sizeof(double) * 3 * (size_t)m.E * (m.p + 1) * (m.p + 1));   // [E][3][n^2]
+  else L.G = take(sizeof(double) * 6 * (size_t)geometry_elems(m.p, m.E) * n3);
   L.dinv = take(sizeof(double) * m.N);
   L.y = take(sizeof(double) * m.N);
   L.t0 = take(sizeof(double) * m.N);
@@ -91,7 +103,7 @@ static sfmg_status level_build(const sfmg_problem* pr, void* d_ws, size_t ws_byt
   sfmg_level_s* lv = new (std::nothrow) sfmg_level_s();
   if (!lv) { set_error("host allocation failed"); return SFMG_E_ARG; }
   lv->prob = *pr; lv->m = m; lv->p = m.p; lv->n = m.p + 1;
-  lv->n3 = (long long)lv->n * lv->n * lv->n; lv->E = m.E; lv->N = m.N;
+  lv->n3 = (long long)lv->n * lv->n * (m.dim == 2 ? 1 : lv->n); lv->E = m.E; lv->N = m.N;
   lv->G = (double*)(base + L.G);
   lv->dinv = (double*)(base + L.dinv);
   lv->y = (double*)(base + L.y);
@@ -107,6 +119,7 @@ static sfmg_status level_build(const sfmg_problem* pr, void* d_ws, size_t ws_byt
   auto fail = [&](sfmg_status st) { delete lv; return st; };
   cudaError_t e;
   if ((e = upload_order_tables(m.p, s))) return fail(cuda_fail(e, "upload_order_tables"));
+  if (m.dim == 2 && (e = upload_2d_tables(m.p, m.quad))) return fail(cuda_fail(e, "upload_2d_tables"));
   if ((e = cudaMemsetAsync(lv->red.counter, 0, sizeof(unsigned int), s))) return fail(cuda_fail(e, "memset"));
   if ((e = cudaMemsetAsync(lv->bad, 0, sizeof(int), s))) return fail(cuda_fail(e, "memset"));
   if ((e = launch_geometry(m, lv->G, lv->bad, s))) return fail(cuda_fail(e, "geometry"));
@@ -151,7 +164,7 @@ static cudaError_t element_kernel(sfmg_level_s* lv, int bc, const double* u, dou
 
 static cudaError_t op_apply(sfmg_level_s* lv, int bc, const double* u, double* v, cudaStream_t s) {
   cudaError_t e;
-  if (lv->p <= 2 && !lv->m.quad) {
+  if (lv->p <= 2 && !lv->m.quad && lv->m.dim == 3) {
     e = cudaMemsetAsync(v, 0, sizeof(double) * lv->N, s);
     if (e) return e;
     return element_kernel(lv, bc, u, v, 1, 1, s);
@@ -358,22 +371,22 @@ sfmg_status sfmg_level_info(sfmg_level lv, int64_t* n_dofs, int64_t* n_elem, int
 }
 
 sfmg_status sfmg_export_l2g(sfmg_level lv, int32_t* d_l2g, void* stream) {
-  if (!lv || !d_l2g) return SFMG_E_ARG;
+  if (!lv || !d_l2g || lv->m.dim == 2) return SFMG_E_ARG;
   CK(launch_export_maps(lv->m, d_l2g, nullptr, nullptr, (cudaStream_t)stream));
   return SFMG_OK;
 }
 sfmg_status sfmg_export_mask(sfmg_level lv, uint8_t* d_mask, void* stream) {
-  if (!lv || !d_mask) return SFMG_E_ARG;
+  if (!lv || !d_mask || lv->m.dim == 2) return SFMG_E_ARG;
   CK(launch_export_maps(lv->m, nullptr, d_mask, nullptr, (cudaStream_t)stream));
   return SFMG_OK;
 }
 sfmg_status sfmg_export_colors(sfmg_level lv, uint8_t* d_col, void* stream) {
-  if (!lv || !d_col) return SFMG_E_ARG;
+  if (!lv || !d_col || lv->m.dim == 2) return SFMG_E_ARG;
   CK(launch_export_maps(lv->m, nullptr, nullptr, d_col, (cudaStream_t)stream));
   return SFMG_OK;
 }
 sfmg_status sfmg_export_geometry(sfmg_level lv, double* d_G, void* stream) {
-  if (!lv || !d_G) return SFMG_E_ARG;
+  if (!lv || !d_G || lv->m.dim == 2) return SFMG_E_ARG;
   CK(launch_export_geometry(lv->m, lv->G, d_G, (cudaStream_t)stream));
   return SFMG_OK;
 }
@@ -394,7 +407,7 @@ sfmg_status sfmg_diag(sfmg_level lv, int32_t bc, double* d_diag, int64_t n, void
 
 sfmg_status sfmg_lambda_max(sfmg_level lv, int32_t iters, uint64_t seed, double* h_lambda, void* stream) {
   if (!lv || !h_lambda || iters < 1) return SFMG_E_ARG;
-  if ((long long)(lv->m.Mx - 2) * (lv->m.My - 2) * (lv->m.Mz - 2) <= 0) {
+  if ((long long)(lv->m.Mx - 2) * (lv->m.My - 2) * (lv->m.dim == 2 ? 1 : lv->m.Mz - 2) <= 0) {
     set_error("level has no interior dofs: D^{-1} A_D is the identity on the boundary");
     return SFMG_E_ARG;
   }
@@ -458,7 +471,7 @@ sfmg_status sfmg_load_vector(sfmg_level lv, int32_t rhs_id, double* d_f, int64_t
 static constexpr int kHostChunks = 8;
 
 static int host_chunks(const sfmg_level_s* lv) {
-  if (lv->m.quad) return 1;
+  if (lv->m.quad || lv->m.dim == 2) return 1;
   if (lv->p <= 2 && ((long long)lv->m.nex * lv->m.ney) % 32 != 0) return 1;   // interleaved G blocks of 32
   if (lv->hp_slabs > 0) return std::min(std::min(lv->hp_slabs, kHostChunks), lv->m.nez);
   const long long plane_bytes = (long long)lv->m.Mx * lv->m.My * 8;
@@ -572,8 +585,10 @@ sfmg_status sfmg_cheb_host(sfmg_level lv, const double* h_b, double* h_x, int64_
 // 1: p pair (fine.p = 2 coarse.p <= 16, same element grid); 2: h pair (same p, fine ne = 2 coarse ne;
 // p = 1: NEXT-1 trilinear gathers, p > 1: NEXT-4 high-order h-transfer)
 static int pair_kind(const MeshDev& c, const MeshDev& f) {
+  if (c.dim != f.dim) return 0;
+  const bool two = f.dim == 2;
   if (f.p == 2 * c.p && c.p <= 8 && f.nex == c.nex && f.ney == c.ney && f.nez == c.nez) return 1;
-  if (c.p == f.p && f.nex == 2 * c.nex && f.ney == 2 * c.ney && f.nez == 2 * c.nez) return 2;
+  if (c.p == f.p && f.nex == 2 * c.nex && f.ney == 2 * c.ney && (two || f.nez == 2 * c.nez)) return 2;
   return 0;
 }
 
@@ -589,12 +604,14 @@ static sfmg_status check_pair(sfmg_level c, sfmg_level f, int* kind) {
 
 static cudaError_t transfer_prolong(const MeshDev& c, const MeshDev& f, const double* uc, double* uf, int add,
                                     cudaStream_t s) {
+  if (f.dim == 2) return launch_transfer_2d(c, f, pair_kind(c, f), 0, uc, uf, add, s);
   if (pair_kind(c, f) == 2)
     return f.p == 1 ? launch_prolong_h(c, f, uc, uf, add, s) : launch_prolong_hp(c, f, uc, uf, add, s);
   return launch_prolong(c, f, uc, uf, add, s);
 }
 static cudaError_t transfer_restrict(const MeshDev& c, const MeshDev& f, const double* rf, double* rc,
                                      cudaStream_t s) {
+  if (f.dim == 2) return launch_transfer_2d(c, f, pair_kind(c, f), 1, rf, rc, 0, s);
   if (pair_kind(c, f) == 2) return f.p == 1 ? launch_restrict_h(c, f, rf, rc, s) : launch_restrict_hp(c, f, rf, rc, s);
   return launch_restrict(c, f, rf, rc, s);
 }
@@ -635,11 +652,13 @@ static sfmg_status hier_specs(const sfmg_problem* fine, const sfmg_mg_params* mg
   }
   for (int j = 1; j <= mg->h_levels; ++j) {
     sfmg_problem pr = out.back();
-    if (pr.nex % 2 || pr.ney % 2 || pr.nez % 2) {
+    const bool two = pr.dim == 2;
+    if (pr.nex % 2 || pr.ney % 2 || (!two && pr.nez % 2)) {
       set_error("mesh cannot be h-coarsened h_levels times (element counts must be divisible by 2^h_levels)");
       return SFMG_E_PCOARSEN;
     }
-    pr.nex /= 2; pr.ney /= 2; pr.nez /= 2;
+    pr.nex /= 2; pr.ney /= 2;
+    if (!two) pr.nez /= 2;
     out.push_back(pr);
   }
   return SFMG_OK;
@@ -737,7 +756,7 @@ sfmg_status sfmg_hier_create(const sfmg_problem* fine, const sfmg_mg_params* mg,
   }
   {
     const MeshDev& mc = h->lv.back()->m;
-    h->host_coarse = !((mc.p == 1 || mc.p == 2));   // single-CTA device CG only for p <= 2 coarse levels
+    h->host_coarse = !((mc.p == 1 || mc.p == 2)) || mc.dim == 2;   // single-CTA device CG: 3-D, p <= 2
   }
   h->lam.assign(h->lv.size(), 0.0);
   for (size_t l = 0; l + 1 < h->lv.size(); ++l) {

@@ -27,6 +27,7 @@ struct MeshDev {
   // mesh; a z-slab view (pipelined host apply) marks an interior cut plane with -1.  Used by the
   // apply and init kernels only.
   int Kb0, Kb1;
+  int dim = 3;             // 3 hexahedra; 2 quadrilaterals (NEXT-2: nez = 1, Mz = 1, Kb0 = Kb1 = -1)
 };
 
 // Device reduction scratch: partials[kRedBlocks][kRedSlots], scalars[32], counter.
@@ -44,6 +45,10 @@ struct Basis1D {
 Basis1D make_basis(int p);
 // I[i*(pc+1)+a] = ell^{pc}_a(x^{pf}_i)
 std::vector<double> make_interp(int pc, int pf);
+// 1-D quadrature tables (k_gauss.cu): LGL nodes xn; B[i*n+a] = ell_a(q_i), DB = ell_a'(q_i), weights qw
+// at the quadrature points q (quad 0: the LGL nodes themselves, quad 1: Gauss-Legendre)
+void quad_tables_1d(int p, int quad, std::vector<double>& xn, std::vector<double>& B, std::vector<double>& DB,
+                    std::vector<double>& qw);
 // h-transfer at order p, child s in {0, 1}: H[i*(p+1)+a] = ell_a((xhat_i + 2 s - 1) / 2)
 std::vector<double> make_h_interp(int p, int s);
 
@@ -128,6 +133,16 @@ cudaError_t launch_diag_gauss(const MeshDev& m, int bc, const double* G, double*
 cudaError_t launch_load_gauss(const MeshDev& m, double* f, cudaStream_t s);
 cudaError_t launch_coarse_cg_gauss(const MeshDev& m, const double* G, const double* b, double* x, double* r,
                                    double* p, double* q, double* scal, double rtol, int maxit, cudaStream_t s);
+
+// ---- 2-D quadrilateral variant (k_2d.cu, NEXT-2); the launchers above dispatch to these when m.dim == 2
+cudaError_t upload_2d_tables(int p, int quad);
+cudaError_t launch_geometry_2d(const MeshDev& m, double* G, int* bad, cudaStream_t s);
+cudaError_t launch_apply_2d(const MeshDev& m, int bc, const double* G, const double* u, double* v, cudaStream_t s);
+cudaError_t launch_diag_2d(const MeshDev& m, int bc, const double* G, double* d, cudaStream_t s);
+cudaError_t launch_load_2d(const MeshDev& m, double* f, cudaStream_t s);
+// 2-D transfer: kind 1 p pair, 2 h pair; dir 0 prolong (out = P0 in, += if add), 1 restrict (out = P0^T in)
+cudaError_t launch_transfer_2d(const MeshDev& mc, const MeshDev& mf, int kind, int dir, const double* in, double* out,
+                               int add, cudaStream_t s);
 
 // ---- vector kernels (k_blas.cu)
 cudaError_t launch_recip(const double* d, double* dinv, long long n, cudaStream_t s);

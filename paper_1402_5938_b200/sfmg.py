@@ -37,7 +37,7 @@ class SfmgError(RuntimeError):
 class _Problem(C.Structure):
     _fields_ = [("nex", C.c_int32), ("ney", C.c_int32), ("nez", C.c_int32), ("order", C.c_int32),
                 ("warp", C.c_int32), ("warp_amp", C.c_double), ("coeff", C.c_int32),
-                ("c0", C.c_double), ("c1", C.c_double), ("quadrature", C.c_int32)]
+                ("c0", C.c_double), ("c1", C.c_double), ("quadrature", C.c_int32), ("dim", C.c_int32)]
 
 
 class _MgParams(C.Structure):
@@ -142,15 +142,16 @@ class Problem:
     c0: float = 1.0
     c1: float = 0.0
     quadrature: int = 0     # 0 collocated LGL (R1), 1 Gauss-Legendre (NEXT-3)
+    dim: int = 3            # 2: quadrilaterals on [0,1]^2 (NEXT-2; nez = 1, coeff 4 = 2d-var')
 
     @classmethod
     def from_dict(cls, d):
         return cls(d["nex"], d["ney"], d["nez"], d["p"], d.get("warp", 0), d.get("amp", 0.0),
-                   d.get("coeff", 0), d.get("c0", 1.0), d.get("c1", 0.0), d.get("quadrature", 0))
+                   d.get("coeff", 0), d.get("c0", 1.0), d.get("c1", 0.0), d.get("quadrature", 0), d.get("dim", 3))
 
     def _c(self):
         return _Problem(self.nex, self.ney, self.nez, self.p, self.warp, self.amp, self.coeff, self.c0, self.c1,
-                        self.quadrature)
+                        self.quadrature, self.dim)
 
 
 def version() -> str:
