@@ -447,6 +447,31 @@ def run_extras(args, sfmg, dev, stream, flush, hbm_peak):
                    "apply_hbm_frac": alg["apply_bytes"] / ta / 1e9 / hbm_peak})
         del lv, u, v
     out["next3_gauss_apply_config3"] = gq
+
+    def timed_solve(prob, mg, mode):
+        H = sfmg.Hierarchy(sfmg.Problem.from_dict(prob), mg, device=dev)
+        bvec = H.levels[0].load_vector(1)
+        H.solve(bvec, mode=mode, rtol=1e-8, max_iter=300)
+        torch.cuda.synchronize()
+        a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        _, rep = H.solve(bvec, mode=mode, rtol=1e-8, max_iter=300)
+        e.record(stream)
+        e.synchronize()
+        r = {"N": H.N, "levels": H.nlevels, "iterations": rep["iterations"], "converged": rep["converged"],
+             "solve_ms": a.elapsed_time(e)}
+        del H
+        return r
+    # NEXT-4: high-order h-multigrid, tab:box / tab:3d-box settings (three meshes at the fine order),
+    # Cheb(3,3) pCG, Gauss quadrature (the paper's) and collocated LGL
+    out["next4_3dconst_hmg_pcg_cheb33"] = {
+        "p%d_%s" % (p, "gauss" if q else "lgl"): timed_solve(dict(inputs.problem(8, p), quadrature=q),
+                                                           sfmg.MgParams.paper_h("cheb", 2), 1)
+        for p in (4, 8) for q in (1, 0)}
+    # NEXT-2: 2d-const 32^2 (tab:box), p-multigrid and h-multigrid Cheb(3,3) pCG, Gauss quadrature
+    out["next2_2dconst_pcg_cheb33"] = {
+        "p%d_%s" % (p, name): timed_solve(dict(nex=32, ney=32, nez=1, p=p, dim=2, quadrature=1), mk("cheb", 2), 1)
+        for p in (4, 16) for name, mk in (("pmg", sfmg.MgParams.paper), ("hmg", sfmg.MgParams.paper_h))}
     return out
 
 
