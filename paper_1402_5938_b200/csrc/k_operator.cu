@@ -31,6 +31,9 @@ namespace sfmg {
 //    -39 % at p = 16) and half the constants.
 //  * c_xw: LGL nodes and weights of every order.
 constexpr int kDCopies = 5;
+#ifndef SFMG_EO_COPIES
+#define SFMG_EO_COPIES 6   // 6: one even-odd table per line pass; 2: one for D, one for D^T
+#endif
 constexpr int dcopies(int P) { return (P % 2 == 1 && P <= 7) ? kDCopies : 1; }
 constexpr int dOffset(int P) {
   int s = 0;
@@ -102,7 +105,7 @@ __device__ __forceinline__ double dmat(int cp, int idx) {
 template <int P, int SET>
 __device__ __forceinline__ void eo_line(const double (&L)[P + 1], double (&out)[P + 1]) {
   constexpr int N = P + 1, c = P / 2;
-  constexpr int base = eoOffset(P) + SET * eoSize(P);
+  constexpr int base = eoOffset(P) + (SFMG_EO_COPIES == 2 ? (SET < 3 ? 0 : 3) : SET) * eoSize(P);
   double ev[c], od[c];
 #pragma unroll
   for (int m = 0; m < c; ++m) {
@@ -264,6 +267,28 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // GS = false: P3 reads the factors straight from L2 into registers (three k-slices in flight);
 //             the whole next-but-one element is TMA-prefetched into L2 (p >= 9: G of one element is
 //             up to 236 KB and cannot be staged).
+#ifndef SFMG_PF_AHEAD
+#define SFMG_PF_AHEAD 1
+#endif
+#ifndef SFMG_RING
+#define SFMG_RING 5
+#endif
+#ifndef SFMG_MINB_HI
+#define SFMG_MINB_HI 1
+#endif
+#ifndef SFMG_EARLY
+#define SFMG_EARLY 1
+#endif
+#ifndef SFMG_V5
+#define SFMG_V5 0            // 1: even p >= 4 through k_apply_v5.cuh (two threads per line; measured slower, kept off)
+#endif
+#ifndef SFMG_V5_SMEM_BUDGET
+#define SFMG_V5_SMEM_BUDGET 60000
+#endif
+#ifndef SFMG_KSTAGE
+#define SFMG_KSTAGE 0
+#endif
+
 template <int P, bool GS>
 struct V4Cfg {
   static constexpr int N = P + 1, N2 = N * N, N3 = N2 * N;
@@ -272,9 +297,14 @@ struct V4Cfg {
   static constexpr int EPB_THR = 256 / N2 > 0 ? 256 / N2 : 1;
   static constexpr int EPB = EPB_SMEM < EPB_THR ? EPB_SMEM : EPB_THR;
   static constexpr int THREADS = EPB * N2;
-  static constexpr size_t SMEM = (size_t)EPB * PER_ELEM + 16;
+  // GS == false with one element per block: the first KST factor k-slices of the element (one contiguous
+  // block of the slice-major layout) are TMA-staged into the smem left free by the work arrays
+  static constexpr int KST_FIT = (232448 - EPB * PER_ELEM - 16) / (6 * N2 * 8);
+  static constexpr int KST_WANT = SFMG_KSTAGE < N ? SFMG_KSTAGE : N;
+  static constexpr int KST = (GS || EPB != 1) ? 0 : (KST_WANT < KST_FIT ? KST_WANT : KST_FIT);
+  static constexpr size_t SMEM = (size_t)EPB * PER_ELEM + (size_t)KST * 6 * N2 * 8 + 16;
   static constexpr int MINB_SMEM = (227 * 1024) / (SMEM + 1024) < 8 ? (227 * 1024) / (SMEM + 1024) : 8;
-  static constexpr int MINB = GS ? MINB_SMEM : (P >= 12 ? 1 : 2);
+  static constexpr int MINB = GS ? MINB_SMEM : (P >= 12 ? SFMG_MINB_HI : 2);
 };
 
 template <int P, bool DIR, bool GS>
@@ -286,7 +316,7 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
   constexpr bool EO = (P % 2 == 0) && P >= 4;   // even-odd line products
   // the next group's u column is loaded right after this group's is staged, so it is in flight
   // during the whole element (measured: p = 16 -2.5 %, p <= 8 within noise)
-  constexpr bool EARLY = true;
+  constexpr bool EARLY = SFMG_EARLY;
   extern __shared__ __align__(128) double smem[];
   double* sG = smem;                                   // [EPB][k][6][n^2] (GS)
   const int le = threadIdx.x / N2;
@@ -294,7 +324,9 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
   const int t0 = t % N, t1 = t / N;
   double* s0 = smem + (GS ? C::EPB * 6 * N3 : 0) + le * 2 * N3;   // per element: s0, su
   double* su = s0 + N3;
-  uint64_t* bar = (uint64_t*)(smem + C::EPB * (GS ? 8 : 2) * N3);
+  constexpr int KST = C::KST;
+  double* sK = smem + C::EPB * (GS ? 8 : 2) * N3;     // [KST][6][n^2] (!GS, EPB == 1)
+  uint64_t* bar = (uint64_t*)(sK + KST * 6 * N2);
   const double* gE = sG + le * 6 * N3;
   const long long sxy = (long long)m.Mx * m.My;
   const long long gstride = gridDim.x;
@@ -338,14 +370,21 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
   };
 
   long long grp = blockIdx.x;
+  // L2 prefetch distance of the factor stream in groups (GS: the TMA already holds group g+1 in smem)
+  constexpr int PF = GS ? 2 : SFMG_PF_AHEAD;
   if (threadIdx.x == 0) {   // factor prefetches need nothing from the predecessor kernel
     if (GS) {
       mbar_init(bar, 1);
       if (grp < ngroups) bulk_load(sG, G + grp * C::EPB * 6 * N3, group_bytes(grp), bar);
-    } else if (grp < ngroups) {
+    } else if (KST > 0) {
+      mbar_init(bar, 1);
+      if (grp < ngroups) bulk_load(sK, G + grp * 6 * N3, KST * 6 * N2 * 8, bar);
+    }
+    if (GS) {
+    } else if (grp < ngroups && PF >= 1) {
       prefetch_group_l2(grp);
     }
-    if (grp + gstride < ngroups) prefetch_group_l2(grp + gstride);
+    if (PF >= 2 && grp + gstride < ngroups) prefetch_group_l2(grp + gstride);
   }
   // wait_mode 2: u is produced by the predecessor; 1: only v is (wait before the first scatter)
   if (wait_mode == 2) pdl_wait();
@@ -367,12 +406,13 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
       bxy = (I == 0) || (I == m.Mx - 1) || (J == 0) || (J == m.My - 1);
     }
     const double* Gg = G + (act ? e : 0) * 6 * N3 + t;   // GS == false: this thread's factor column
-    double gb[3][6];                                        // GS == false: k-slice ring in registers
+    constexpr int RG = SFMG_RING;                           // ring depth (loads RG - 1 slices ahead)
+    double gb[RG][6];                                       // GS == false: k-slice ring in registers
     if (!GS) {
 #pragma unroll
-      for (int kk = 0; kk < 2 && kk < N; ++kk)
+      for (int kk = 0; kk < RG - 1 && KST + kk < N; ++kk)
 #pragma unroll
-        for (int c = 0; c < 6; ++c) gb[kk][c] = __ldcs(Gg + gofs<N>(c, 0, kk));
+        for (int c = 0; c < 6; ++c) gb[kk][c] = __ldcs(Gg + gofs<N>(c, 0, KST + kk));
     }
 #pragma unroll
     for (int k = 0; k < N; ++k) su[t + N2 * k] = ru[k];
@@ -422,7 +462,7 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
       }
     }
     __syncthreads();
-    if (GS) {
+    if (GS || KST > 0) {
       mbar_wait(bar, phase);
       phase ^= 1u;
     }
@@ -443,16 +483,18 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
 #pragma unroll
       for (int k = 0; k < N; ++k) {
         double G00, G01, G02, G11, G12, G22;
-        if (GS) {
-          const double* Gk = gE + gofs<N>(0, t, k);
+        if (GS || k < KST) {
+          const double* Gk = (GS ? gE : sK) + gofs<N>(0, t, k);
           G00 = Gk[0]; G01 = Gk[N2]; G02 = Gk[2 * N2]; G11 = Gk[3 * N2]; G12 = Gk[4 * N2]; G22 = Gk[5 * N2];
         } else {
-          if (k + 2 < N) {
+          constexpr int zk = 0;
+          const int kr = k - KST + zk;   // ring slot index (compile-time after unrolling)
+          if (k + RG - 1 < N) {
 #pragma unroll
-            for (int c = 0; c < 6; ++c) gb[(k + 2) % 3][c] = __ldcs(Gg + gofs<N>(c, 0, k + 2));
+            for (int c = 0; c < 6; ++c) gb[(kr + RG - 1) % RG][c] = __ldcs(Gg + gofs<N>(c, 0, k + RG - 1));
           }
-          G00 = gb[k % 3][0]; G01 = gb[k % 3][1]; G02 = gb[k % 3][2];
-          G11 = gb[k % 3][3]; G12 = gb[k % 3][4]; G22 = gb[k % 3][5];
+          G00 = gb[kr % RG][0]; G01 = gb[kr % RG][1]; G02 = gb[kr % RG][2];
+          G11 = gb[kr % RG][3]; G12 = gb[kr % RG][4]; G22 = gb[kr % RG][5];
         }
         const int idx = t + N2 * k;
         const double g0 = s0[idx], g1 = su[idx], g2 = g2a[k];
@@ -479,8 +521,12 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
         if (GS) {
           fence_proxy_async_smem();
           bulk_load(sG, G + nx * C::EPB * 6 * N3, group_bytes(nx), bar);
+        } else if (KST > 0) {
+          fence_proxy_async_smem();
+          bulk_load(sK, G + nx * 6 * N3, KST * 6 * N2 * 8, bar);
         }
-        if (nx + gstride < ngroups) prefetch_group_l2(nx + gstride);
+        if (PF >= 2 && nx + gstride < ngroups) prefetch_group_l2(nx + gstride);
+        else if (PF == 1 && nx < ngroups) prefetch_group_l2(nx);
       }
     }
     if (!EARLY && grp + gstride < ngroups) {   // next group's u column, in flight during P4-P6
@@ -545,6 +591,8 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
     for (int k = 0; k < N; ++k) ru[k] = rn[k];
   }
 }
+
+#include "k_apply_v5.cuh"
 
 // ------------------------------------------------------------------------------------------
 // K2 apply, thread per element (p <= 2): the whole element (n^3 <= 27 nodes) lives in registers,
@@ -1064,6 +1112,26 @@ static cudaError_t apply_pd(const MeshDev& m, const double* G, const double* u, 
     long long blocks = (m.E + 127) / 128;
     if (blocks > grid) blocks = grid;
     return launch_pdl(k_apply_tpe<P, DIR>, (unsigned)blocks, 128, 0, s, m, G, u, v, wait_mode, write_bnd);
+  } else if constexpr (SFMG_V5 && P % 2 == 0 && P >= 4) {
+    constexpr bool GS = (P <= 8);
+    using C = V5Cfg<P, GS>;
+    static int resident = 0;
+    static int num_sms = 0;
+    if (!resident) {
+      cudaError_t e = cudaFuncSetAttribute(k_apply_v5<P, DIR, GS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+      if (e) return e;
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_apply_v5<P, DIR, GS>, C::THREADS, C::SMEM);
+      if (e) return e;
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+      if (resident < 1) resident = 1;
+    }
+    const long long groups = (m.E + C::EPB - 1) / C::EPB;
+    long long grid = (long long)resident * num_sms;
+    if (grid > groups) grid = groups;
+    return launch_pdl(k_apply_v5<P, DIR, GS>, (unsigned)grid, (unsigned)C::THREADS, C::SMEM, s, m, G, u, v, groups,
+                      wait_mode, write_bnd);
   } else {
     constexpr bool GS = (P <= 8);
     using C = V4Cfg<P, GS>;

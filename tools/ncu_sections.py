@@ -1,6 +1,6 @@
 """Per-section split of an ncu report (source page): executed instructions and warp-stall samples
-between consecutive block barriers / mbarrier waits of a kernel.  Developer tool:
-python tools/ncu_sections.py report.ncu-rep"""
+(total and the top stall reasons) between consecutive block barriers / mbarrier waits of a kernel.
+Developer tool: python tools/ncu_sections.py report.ncu-rep"""
 import csv
 import subprocess
 import sys
@@ -10,14 +10,27 @@ out = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-s
 rows = list(csv.reader(out.splitlines()))
 hdr = rows[1]
 isrc, iex, ismp = hdr.index("Source"), hdr.index("Instructions Executed"), hdr.index("Warp Stall Sampling (All Samples)")
+reasons = [(i, h[6:]) for i, h in enumerate(hdr) if h.startswith("stall_") and "Not Issued" not in h]
 body = [r for r in rows[2:] if len(r) == len(hdr)]
-tot = sum(int(r[iex] or 0) for r in body); stot = sum(int(r[ismp] or 0) for r in body)
-sec, acc, sacc, start = 0, 0, 0, body[0][isrc]
-cnt = 0
+num = lambda x: int(float(x or 0))
+tot = sum(num(r[iex]) for r in body)
+stot = sum(num(r[ismp]) for r in body)
+
+
+def flush(sec, cnt, acc, sacc, rs, end):
+    top = sorted(rs.items(), key=lambda kv: -kv[1])[:4]
+    tops = " ".join("%s %.1f" % (k, 100.0 * v / stot) for k, v in top if v > 0)
+    print("sect %2d: %5d instr static, %5.1f%% executed, %5.1f%% stall samples [%s]  (ends %s)"
+          % (sec, cnt, 100.0 * acc / tot, 100.0 * sacc / stot, tops, end[:40]))
+
+
+sec, acc, sacc, cnt, rs = 0, 0, 0, 0, {}
 for r in body:
     src = r[isrc].strip()
-    acc += int(r[iex] or 0); sacc += int(r[ismp] or 0); cnt += 1
+    acc += num(r[iex]); sacc += num(r[ismp]); cnt += 1
+    for i, name in reasons:
+        rs[name] = rs.get(name, 0) + num(r[i])
     if "BAR.SYNC" in src or "SYNCS.PHASECHK" in src or "EXIT" in src:
-        print("sect %2d: %5d instr static, %5.1f%% executed, %5.1f%% stall samples  (ends %s)" % (sec, cnt, 100.0*acc/tot, 100.0*sacc/stot, src[:40]))
-        sec += 1; acc = 0; sacc = 0; cnt = 0
-print("tail: %d static %.1f%% exec %.1f%% samples" % (cnt, 100.0*acc/tot, 100.0*sacc/stot))
+        flush(sec, cnt, acc, sacc, rs, src)
+        sec += 1; acc = 0; sacc = 0; cnt = 0; rs = {}
+flush(sec, cnt, acc, sacc, rs, "tail")
