@@ -215,12 +215,32 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 
+// The geometric factors are the one stream read exactly once per apply (48 B per point, ~80 % of the
+// bytes); their bulk copies and L2 prefetches carry an L2 evict-first policy so that the streamed
+// factors do not push u and the RED target v (each touched by up to 8 elements, at different times)
+// out of L2.
+#ifndef SFMG_G_EVICT_FIRST
+#define SFMG_G_EVICT_FIRST 1
+#endif
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
+  if (SFMG_G_EVICT_FIRST) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(l2_evict_first_policy())
+        : "memory");
+  } else {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+  }
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
@@ -231,8 +251,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
       : "memory");
 }
 
+#ifndef SFMG_G_EF_PREFETCH
+#define SFMG_G_EF_PREFETCH SFMG_G_EVICT_FIRST
+#endif
 __device__ __forceinline__ void bulk_prefetch_l2(const void* src, unsigned bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+  if (SFMG_G_EF_PREFETCH) {
+    asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(src), "r"(bytes),
+                 "l"(l2_evict_first_policy())
+                 : "memory");
+  } else {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+  }
 }
 
 __device__ __forceinline__ void fence_proxy_async_smem() {
@@ -272,6 +301,9 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 #endif
 #ifndef SFMG_RING
 #define SFMG_RING 5
+#endif
+#ifndef SFMG_PF_TOP
+#define SFMG_PF_TOP 0
 #endif
 #ifndef SFMG_MINB_HI
 #define SFMG_MINB_HI 1
@@ -316,7 +348,8 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
   constexpr bool EO = (P % 2 == 0) && P >= 4;   // even-odd line products
   // the next group's u column is loaded right after this group's is staged, so it is in flight
   // during the whole element (measured: p = 16 -2.5 %, p <= 8 within noise)
-  constexpr bool EARLY = SFMG_EARLY;
+  // (p >= 12: off; the u columns are L2-prefetched instead, which frees 2n registers: p = 16 -2 %)
+  constexpr bool EARLY = (P >= 12) ? (SFMG_EARLY > 1) : (SFMG_EARLY > 0);
   extern __shared__ __align__(128) double smem[];
   double* sG = smem;                                   // [EPB][k][6][n^2] (GS)
   const int le = threadIdx.x / N2;
@@ -405,6 +438,8 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
       const int I = ex * P + t0, J = ey * P + t1;
       bxy = (I == 0) || (I == m.Mx - 1) || (J == 0) || (J == m.My - 1);
     }
+    if (!GS && PF == 1 && SFMG_PF_TOP && threadIdx.x == 0 && grp + gstride < ngroups)
+      prefetch_group_l2(grp + gstride);   // next group's factors, a whole element ahead
     const double* Gg = G + (act ? e : 0) * 6 * N3 + t;   // GS == false: this thread's factor column
     constexpr int RG = SFMG_RING;                           // ring depth (loads RG - 1 slices ahead)
     double gb[RG][6];                                       // GS == false: k-slice ring in registers
@@ -526,7 +561,7 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
           bulk_load(sK, G + nx * 6 * N3, KST * 6 * N2 * 8, bar);
         }
         if (PF >= 2 && nx + gstride < ngroups) prefetch_group_l2(nx + gstride);
-        else if (PF == 1 && nx < ngroups) prefetch_group_l2(nx);
+        else if (PF == 1 && !SFMG_PF_TOP && nx < ngroups) prefetch_group_l2(nx);
       }
     }
     if (!EARLY && grp + gstride < ngroups) {   // next group's u column, in flight during P4-P6
