@@ -5,7 +5,9 @@ for p = 1..16; Chebyshev-Jacobi step time).
 Default (N=1): BASELINE config 2 (configs[1]) -- 16^3 deformed hexes, p = 8, mu = exp(3S),
 u uniform in [-1,1] from seed 1.  One step = one A_D u apply + one degree-4 Chebyshev-Jacobi
 application (b = 0, x0 = u, R16) = 5 operator applies.  `value` = N / (mean apply time) in GDoF/s.
-Between timed steps the L2 is flushed (a 512 MB write).  Extra keys report the config-3 p-sweep,
+Between timed steps the L2 is flushed: a 512 MB write, then a read of the same buffer, so the L2 holds
+no data of the workload and no dirty flush lines are written back inside the timed region (the
+write-only flush's write-back costs the config-2 apply ~3 us; that number is reported too).  Extra keys report the config-3 p-sweep,
 config 4 (135 M dofs) and the config-5 p-MG preconditioned CG solve measured in the same run.
 
 Launch: python bench.py [--gpus N --steps K --warmup W] [--impl reference]
@@ -253,7 +255,7 @@ def run_gpu(args, rank, world, local_rank):
         t_end = torch.cuda.Event(enable_timing=True)
         t_start.record(stream)
         for k in range(args.steps):
-            flush.fill_(float(k))           # L2 flush between timed steps (not in the step time)
+            l2_flush(flush, k)              # L2 flush between timed steps (not in the step time)
             step(evs[k])
         t_end.record(stream)
         barrier()
@@ -269,7 +271,7 @@ def run_gpu(args, rank, world, local_rank):
     lv.profile(True)
     kreps = max(3, min(args.steps, 50))
     for k in range(kreps):
-        flush.fill_(float(k))
+        l2_flush(flush, k)
         step([torch.cuda.Event(enable_timing=True) for _ in range(4)])
     torch.cuda.synchronize()
     k_ms, k_launches = lv.profile_read(reset=True)
@@ -289,6 +291,11 @@ def run_gpu(args, rank, world, local_rank):
                       % (k_launches, t_kernel * 1e6),
             "peak_kind": peak_kind, "algorithmic_bytes_per_launch": alg["apply_bytes"],
             "abi_apply_us": t_apply * 1e6, "abi_apply_frac": alg["apply_bytes"] / t_apply / 1e9 / hbm_peak}
+
+    # the same ABI apply after a write-only flush (the flush's dirty lines are written back inside the
+    # timed region): reported next to `value` for transparency
+    t_apply_dirty = max_over_ranks(time_events(lambda: lv.apply(u, v), stream, None, 20, warm=3,
+                                               flush_fn=lambda k: l2_flush(flush, k, read=False)))
 
     # ---------------- end to end through the host-buffer ABI (pinned host in, host out)
     v_host = torch.empty(N, dtype=torch.float64).pin_memory()
@@ -314,9 +321,10 @@ def run_gpu(args, rank, world, local_rank):
            "config": {"workload": "BASELINE config 2: 16^3 deformed hexes (x+0.1 sin sin sin), p=8, "
                                   "mu=exp(3 sin2pix sin2piy sin2piz), N=129^3, u~U[-1,1] seed 1; step = A_D u + "
                                   "one degree-4 Chebyshev-Jacobi application (b=0, x0=u)",
-                      "l2": "flushed between timed steps (512 MB write)", "parallelism": "replicas" if world > 1
+                      "l2": "flushed between timed steps (512 MB write, then a read of it: clean lines)",
+                      "parallelism": "replicas" if world > 1
                       else "single GPU"},
-           "apply_ms": t_apply * 1e3, "cheb_step_ms": t_cheb / 4 * 1e3,
+           "apply_ms": t_apply * 1e3, "apply_ms_write_only_flush": t_apply_dirty * 1e3, "cheb_step_ms": t_cheb / 4 * 1e3,
            "cheb_step_gdofs": world * N / (t_cheb / 4) / 1e9,
            "cheb_step_hbm_frac": alg["step_bytes"] / (t_cheb / 4) / 1e9 / hbm_peak,
            "apply_tflops": alg["apply_flops"] / t_apply / 1e12,
@@ -336,15 +344,25 @@ def run_gpu(args, rank, world, local_rank):
         print(json.dumps(out), flush=True)
 
 
-def time_events(fn, stream, flush, reps, warm=3):
+def l2_flush(flush, k, read=True):
+    """Evict the workload from L2 between timed steps: write a buffer larger than L2, then read it
+    back so the lines left in L2 are clean (no write-back of flush data inside the timed region)."""
+    flush.fill_(float(k))
+    if read:
+        flush.sum()
+
+
+def time_events(fn, stream, flush, reps, warm=3, flush_fn=None):
     import torch
     for _ in range(warm):
         fn()
     torch.cuda.synchronize()
     ts = []
     for k in range(reps):
-        if flush is not None:
-            flush.fill_(float(k))
+        if flush_fn is not None:
+            flush_fn(k)
+        elif flush is not None:
+            l2_flush(flush, k)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
         fn()

@@ -302,6 +302,12 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 #ifndef SFMG_RING
 #define SFMG_RING 5
 #endif
+#ifndef SFMG_PF_GS
+#define SFMG_PF_GS 2   // GS: TMA holds group g+1; L2 prefetch of g+2 (3: also g+3)
+#endif
+#ifndef SFMG_PF_START
+#define SFMG_PF_START 0   // 0: no L2 prefetch burst at kernel start (steady-state prefetches only)
+#endif
 #ifndef SFMG_PF_TOP
 #define SFMG_PF_TOP 0
 #endif
@@ -404,7 +410,11 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
 
   long long grp = blockIdx.x;
   // L2 prefetch distance of the factor stream in groups (GS: the TMA already holds group g+1 in smem)
-  constexpr int PF = GS ? 2 : SFMG_PF_AHEAD;
+  // L2 prefetch distance of the factor stream in groups.  GS: the TMA already holds group g+1 in smem;
+  // an L2 prefetch of g+2 deepens the HBM pipeline, which pays in long runs (config 4: 2.68 -> 2.53 ms)
+  // but delays the first TMA loads of short ones (config 2: 46.1 -> 48.1 us), so it is used only when
+  // each block walks >= 16 groups.  !GS: g+1 (two generations of p >= 9 factors overflow L2).
+  const int PF = GS ? (SFMG_PF_GS >= 2 && ngroups >= 16 * gstride ? SFMG_PF_GS : 1) : SFMG_PF_AHEAD;
   if (threadIdx.x == 0) {   // factor prefetches need nothing from the predecessor kernel
     if (GS) {
       mbar_init(bar, 1);
@@ -417,7 +427,8 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
     } else if (grp < ngroups && PF >= 1) {
       prefetch_group_l2(grp);
     }
-    if (PF >= 2 && grp + gstride < ngroups) prefetch_group_l2(grp + gstride);
+    if (SFMG_PF_START && PF >= 2 && grp + gstride < ngroups) prefetch_group_l2(grp + gstride);
+    if (SFMG_PF_START && PF >= 3 && grp + 2 * gstride < ngroups) prefetch_group_l2(grp + 2 * gstride);
   }
   // wait_mode 2: u is produced by the predecessor; 1: only v is (wait before the first scatter)
   if (wait_mode == 2) pdl_wait();
@@ -560,8 +571,9 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
           fence_proxy_async_smem();
           bulk_load(sK, G + nx * 6 * N3, KST * 6 * N2 * 8, bar);
         }
-        if (PF >= 2 && nx + gstride < ngroups) prefetch_group_l2(nx + gstride);
-        else if (PF == 1 && !SFMG_PF_TOP && nx < ngroups) prefetch_group_l2(nx);
+        if (PF >= 3 && nx + 2 * gstride < ngroups) prefetch_group_l2(nx + 2 * gstride);
+        else if (PF == 2 && nx + gstride < ngroups) prefetch_group_l2(nx + gstride);
+        else if (!GS && PF == 1 && !SFMG_PF_TOP && nx < ngroups) prefetch_group_l2(nx);
       }
     }
     if (!EARLY && grp + gstride < ngroups) {   // next group's u column, in flight during P4-P6

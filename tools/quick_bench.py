@@ -20,7 +20,11 @@ def timeit(fn, reps=40, warm=3, flush=None):
     ts = []
     for _ in range(reps):
         if flush is not None:
-            flush.fill_(1.0)
+            mode = os.environ.get("QB_FLUSH", "writeread")
+            if mode in ("write", "writeread"):
+                flush.fill_(1.0)
+            if mode in ("read", "writeread"):
+                flush.sum()   # leaves clean lines in L2: no dirty write-back inside the timed region
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         fn()
