@@ -302,6 +302,12 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 #ifndef SFMG_RING
 #define SFMG_RING 5
 #endif
+#ifndef SFMG_V4_SMEM
+#define SFMG_V4_SMEM 52000   // smem budget per block that sets the elements per block (p <= 8)
+#endif
+#ifndef SFMG_V4_THR
+#define SFMG_V4_THR 256
+#endif
 #ifndef SFMG_PF_GS
 #define SFMG_PF_GS 2   // GS: TMA holds group g+1; L2 prefetch of g+2 (3: also g+3)
 #endif
@@ -331,8 +337,8 @@ template <int P, bool GS>
 struct V4Cfg {
   static constexpr int N = P + 1, N2 = N * N, N3 = N2 * N;
   static constexpr int PER_ELEM = (GS ? 8 : 2) * N3 * 8;   // smem bytes per element
-  static constexpr int EPB_SMEM = 52000 / PER_ELEM > 0 ? 52000 / PER_ELEM : 1;
-  static constexpr int EPB_THR = 256 / N2 > 0 ? 256 / N2 : 1;
+  static constexpr int EPB_SMEM = SFMG_V4_SMEM / PER_ELEM > 0 ? SFMG_V4_SMEM / PER_ELEM : 1;
+  static constexpr int EPB_THR = SFMG_V4_THR / N2 > 0 ? SFMG_V4_THR / N2 : 1;
   static constexpr int EPB = EPB_SMEM < EPB_THR ? EPB_SMEM : EPB_THR;
   static constexpr int THREADS = EPB * N2;
   // GS == false with one element per block: the first KST factor k-slices of the element (one contiguous
