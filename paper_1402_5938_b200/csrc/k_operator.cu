@@ -1282,12 +1282,127 @@ cudaError_t launch_export_maps(const MeshDev& m, int32_t* l2g, uint8_t* mask, ui
 }
 
 constexpr int kCoarseThreads = 512;
+// Coarse p = 1 CG with the operator as a 27-point stencil in registers (N <= 768 lattice nodes, one
+// thread per node).  Each thread first assembles its row of A_D = M A M + (I - M) from the <= 8
+// elements around its node: K_e[l][m] = sum_q (grad phi_l)(q)^T G_q (grad phi_m)(q) with the collocated
+// p = 1 gradients (D from __constant__, G in the element-interleaved p <= 2 layout), columns of
+// boundary nodes dropped (R4).  The CG iteration is then one 27-term register x shared-memory product
+// per row and two block reductions -- the same unpreconditioned CG, x0 = 0, ||r|| <= rtol ||b|| (R13),
+// as k_coarse_cg_smem, which re-ran the element apply (48 factor loads per element) every iteration.
+#ifndef SFMG_COARSE_STENCIL
+#define SFMG_COARSE_STENCIL 1
+#endif
+constexpr int kStencilThreads = 768;
+__global__ void __launch_bounds__(kStencilThreads) k_coarse_cg_stencil(MeshDev m, const double* __restrict__ G,
+                                                                        const double* __restrict__ b,
+                                                                        double* __restrict__ xout, double* scal,
+                                                                        double rtol, int maxit) {
+  using GL = GLayout<1>;
+  __shared__ double sp[kStencilThreads];
+  __shared__ double red[32];
+  const int g = threadIdx.x;
+  const bool live = g < m.N;
+  const int Mx = m.Mx, My = m.My, Mz = m.Mz;
+  int I = 0, J = 0, K = 0;
+  if (live) {
+    I = g % Mx;
+    J = (g / Mx) % My;
+    K = g / (Mx * My);
+  }
+  auto interior = [&](int i, int j, int k) { return i > 0 && i < Mx - 1 && j > 0 && j < My - 1 && k > 0 && k < Mz - 1; };
+  const bool inner = live && interior(I, J, K);
+  double S[27];
+#pragma unroll
+  for (int d = 0; d < 27; ++d) S[d] = 0.0;
+  if (inner) {
+#pragma unroll
+    for (int dz = 0; dz < 2; ++dz)
+#pragma unroll
+      for (int dy = 0; dy < 2; ++dy)
+#pragma unroll
+        for (int dx = 0; dx < 2; ++dx) {
+          const int ex = I - 1 + dx, ey = J - 1 + dy, ez = K - 1 + dz;   // element; node is its local (a, b, c)
+          constexpr int zero = 0;
+          const int a = 1 - dx + zero, bb = 1 - dy + zero, c = 1 - dz + zero;
+          const long long e = ex + (long long)m.nex * (ey + (long long)m.ney * ez);
+#pragma unroll
+          for (int k = 0; k < 2; ++k)
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+#pragma unroll
+              for (int i = 0; i < 2; ++i) {
+                const int ij = i + 2 * j;
+                const double G00 = __ldg(G + GL::off(e, 0, ij, k)), G01 = __ldg(G + GL::off(e, 1, ij, k));
+                const double G02 = __ldg(G + GL::off(e, 2, ij, k)), G11 = __ldg(G + GL::off(e, 3, ij, k));
+                const double G12 = __ldg(G + GL::off(e, 4, ij, k)), G22 = __ldg(G + GL::off(e, 5, ij, k));
+                // grad phi_l at q = (i, j, k) for l = (a, bb, c)
+                const double l0 = (j == bb && k == c) ? dmat<1>(0, i * 2 + a) : 0.0;
+                const double l1 = (i == a && k == c) ? dmat<1>(0, j * 2 + bb) : 0.0;
+                const double l2 = (i == a && j == bb) ? dmat<1>(0, k * 2 + c) : 0.0;
+                const double w0 = G00 * l0 + G01 * l1 + G02 * l2;
+                const double w1 = G01 * l0 + G11 * l1 + G12 * l2;
+                const double w2 = G02 * l0 + G12 * l1 + G22 * l2;
+#pragma unroll
+                for (int c2 = 0; c2 < 2; ++c2)
+#pragma unroll
+                  for (int b2 = 0; b2 < 2; ++b2)
+#pragma unroll
+                    for (int a2 = 0; a2 < 2; ++a2) {
+                      const double m0 = (j == b2 && k == c2) ? dmat<1>(0, i * 2 + a2) : 0.0;
+                      const double m1 = (i == a2 && k == c2) ? dmat<1>(0, j * 2 + b2) : 0.0;
+                      const double m2 = (i == a2 && j == b2) ? dmat<1>(0, k * 2 + c2) : 0.0;
+                      const int d = (a2 - a + 1) + 3 * (b2 - bb + 1) + 9 * (c2 - c + 1);
+                      const bool col = interior(ex + a2, ey + b2, ez + c2);
+                      S[d] += col ? (w0 * m0 + w1 * m1 + w2 * m2) : 0.0;
+                    }
+              }
+        }
+  }
+  double x = 0.0, r = live ? b[g] : 0.0, p = r;
+  sp[g] = p;
+  double rr = block_sum(r * r, red);
+  const double bn = sqrt(rr);
+  int it = 0, status = 0;
+  if (bn > 0.0) {
+    for (; it < maxit; ++it) {
+      if (sqrt(rr) <= rtol * bn) break;
+      __syncthreads();
+      double q = p;   // boundary rows: identity
+      if (inner) {
+        q = 0.0;
+#pragma unroll
+        for (int d = 0; d < 27; ++d) {
+          const int ox = d % 3 - 1, oy = (d / 3) % 3 - 1, oz = d / 9 - 1;
+          q = fma(S[d], sp[g + ox + Mx * (oy + My * oz)], q);
+        }
+      } else if (!live) {
+        q = 0.0;
+      }
+      const double pq = block_sum(p * q, red);
+      if (!(pq > 0.0)) { status = 6; break; }
+      const double alpha = rr / pq;
+      x += alpha * p;
+      r -= alpha * q;
+      const double rn = block_sum(r * r, red);
+      p = r + (rn / rr) * p;
+      sp[g] = p;   // every read of the old p is before the reductions' barriers
+      rr = rn;
+    }
+  }
+  if (live) xout[g] = x;
+  if (threadIdx.x == 0) { scal[8] = (double)it; scal[9] = sqrt(rr); scal[10] = (double)status; }
+}
+
 constexpr long long kCoarseSmemN = 6400;   // x, r, p, q of up to this many dofs live in shared memory
 
 cudaError_t launch_coarse_cg(const MeshDev& m, const double* G, const double* b, double* x, double* r,
                              double* p, double* q, double* scal, double rtol, int maxit, cudaStream_t s) {
   if (m.quad) return launch_coarse_cg_gauss(m, G, b, x, r, p, q, scal, rtol, maxit, s);
   if (m.p != 1 && m.p != 2) return cudaErrorInvalidValue;
+  if (SFMG_COARSE_STENCIL && m.p == 1 && m.dim == 3 && m.N <= kStencilThreads) {
+    k_coarse_cg_stencil<<<1, kStencilThreads, 0, s>>>(m, G, b, x, scal, rtol, maxit);
+    return cudaGetLastError();
+  }
   if (m.N <= kCoarseSmemN) {
     const size_t smem = sizeof(double) * 4 * (size_t)m.N;
     static bool attr1 = false, attr2 = false;

@@ -43,8 +43,10 @@ struct XferCfg {
   static constexpr int NC3 = NC * NC * NC, NF3 = NF * NF * NF;
   static constexpr int T1 = NF * NC * NC, T2 = NF * NF * NC;      // prolong intermediates
   static constexpr int R1 = NC * NF * NF, R2 = NC * NC * NF;      // restrict intermediates
-  static constexpr size_t SMEM_P = sizeof(double) * (NC3 + T1 + T2);
-  static constexpr size_t SMEM_R = sizeof(double) * (NF3 + R1 + R2);
+  // + the 1-D interpolation matrix: every pass indexes it by a thread-dependent row, which from
+  // __constant__ memory would serialise the warp over its distinct addresses
+  static constexpr size_t SMEM_P = sizeof(double) * (NC3 + T1 + T2 + NF * NC);
+  static constexpr size_t SMEM_R = sizeof(double) * (NF3 + R1 + R2 + NF * NC);
 };
 
 template <int PC>
@@ -56,7 +58,8 @@ __global__ void __launch_bounds__(256) k_prolong(MeshDev mc, MeshDev mf, const d
   double* sc = sm;             // [c][b][a]
   double* t1 = sc + C::NC3;    // [c][b][i]
   double* t2 = t1 + C::T1;     // [c][j][i]
-  const double* I = c_I[PC - 1];
+  double* I = t2 + C::T2;      // [i][a]
+  for (int l = threadIdx.x; l < NF * NC; l += blockDim.x) I[l] = c_I[PC - 1][l];
   const long long e = blockIdx.x;
   int ex, ey, ez;
   ecoords(mf, e, ex, ey, ez);
@@ -109,7 +112,8 @@ __global__ void __launch_bounds__(256) k_restrict(MeshDev mc, MeshDev mf, const 
   double* sf = sm;             // [k][j][i]
   double* t1 = sf + C::NF3;    // [k][j][a]
   double* t2 = t1 + C::R1;     // [k][b][a]
-  const double* I = c_I[PC - 1];
+  double* I = t2 + C::R2;      // [i][a]
+  for (int l = threadIdx.x; l < NF * NC; l += blockDim.x) I[l] = c_I[PC - 1][l];
   const long long e = blockIdx.x;
   int ex, ey, ez;
   ecoords(mf, e, ex, ey, ez);
