@@ -1293,6 +1293,18 @@ constexpr int kCoarseThreads = 512;
 #define SFMG_COARSE_STENCIL 1
 #endif
 constexpr int kStencilThreads = 768;
+// block-wide sum for the single-CTA CG: warp shuffles, one partial per warp in smem, then every warp
+// reduces the <= 32 partials with shuffles (no serial chain over the partials)
+__device__ __forceinline__ double block_sum_fast(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+  __syncthreads();
+  if (ln == 0) red[w] = v;
+  __syncthreads();
+  double s = ln < (int)((blockDim.x + 31) >> 5) ? red[ln] : 0.0;
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  return s;
+}
 __global__ void __launch_bounds__(kStencilThreads) k_coarse_cg_stencil(MeshDev m, const double* __restrict__ G,
                                                                         const double* __restrict__ b,
                                                                         double* __restrict__ xout, double* scal,
@@ -1360,7 +1372,7 @@ __global__ void __launch_bounds__(kStencilThreads) k_coarse_cg_stencil(MeshDev m
   }
   double x = 0.0, r = live ? b[g] : 0.0, p = r;
   sp[g] = p;
-  double rr = block_sum(r * r, red);
+  double rr = block_sum_fast(r * r, red);
   const double bn = sqrt(rr);
   int it = 0, status = 0;
   if (bn > 0.0) {
@@ -1369,21 +1381,22 @@ __global__ void __launch_bounds__(kStencilThreads) k_coarse_cg_stencil(MeshDev m
       __syncthreads();
       double q = p;   // boundary rows: identity
       if (inner) {
-        q = 0.0;
+        double q3[3] = {0.0, 0.0, 0.0};   // one partial sum per z offset (three short FMA chains)
 #pragma unroll
         for (int d = 0; d < 27; ++d) {
           const int ox = d % 3 - 1, oy = (d / 3) % 3 - 1, oz = d / 9 - 1;
-          q = fma(S[d], sp[g + ox + Mx * (oy + My * oz)], q);
+          q3[d / 9] = fma(S[d], sp[g + ox + Mx * (oy + My * oz)], q3[d / 9]);
         }
+        q = (q3[0] + q3[1]) + q3[2];
       } else if (!live) {
         q = 0.0;
       }
-      const double pq = block_sum(p * q, red);
+      const double pq = block_sum_fast(p * q, red);
       if (!(pq > 0.0)) { status = 6; break; }
       const double alpha = rr / pq;
       x += alpha * p;
       r -= alpha * q;
-      const double rn = block_sum(r * r, red);
+      const double rn = block_sum_fast(r * r, red);
       p = r + (rn / rr) * p;
       sp[g] = p;   // every read of the old p is before the reductions' barriers
       rr = rn;

@@ -43,11 +43,17 @@ struct XferCfg {
   static constexpr int NC3 = NC * NC * NC, NF3 = NF * NF * NF;
   static constexpr int T1 = NF * NC * NC, T2 = NF * NF * NC;      // prolong intermediates
   static constexpr int R1 = NC * NF * NF, R2 = NC * NC * NF;      // restrict intermediates
-  // + the 1-D interpolation matrix: every pass indexes it by a thread-dependent row, which from
-  // __constant__ memory would serialise the warp over its distinct addresses
-  static constexpr size_t SMEM_P = sizeof(double) * (NC3 + T1 + T2 + NF * NC);
-  static constexpr size_t SMEM_R = sizeof(double) * (NF3 + R1 + R2 + NF * NC);
+  static constexpr size_t SMEM_P = sizeof(double) * (NC3 + T1 + T2 + NF * NC);   // + I (k_prolong)
+  static constexpr size_t SMEM_R = sizeof(double) * (NF3 + R1 + R2);
 };
+
+// Prolongation: thread per output value in each pass, I copied to shared memory (a thread-dependent
+// row index into __constant__ memory serialises the warp).  Restriction: one thread per 1-D line in
+// each pass; every thread runs the same unrolled loop over the line's outputs, so each I[i][a] is a
+// compile-time __constant__ operand (uniform across the warp) and each input is loaded once per line
+// (measured, cold: restrict<8> 43 -> 31 us; the line form of the prolongation needs 167 registers and
+// is slower, 53 vs 35 us).
+constexpr int kXferThreads = 320;
 
 template <int PC>
 __global__ void __launch_bounds__(256) k_prolong(MeshDev mc, MeshDev mf, const double* __restrict__ uc,
@@ -104,16 +110,15 @@ __global__ void __launch_bounds__(256) k_prolong(MeshDev mc, MeshDev mf, const d
 }
 
 template <int PC>
-__global__ void __launch_bounds__(256) k_restrict(MeshDev mc, MeshDev mf, const double* __restrict__ rf,
-                                                  double* __restrict__ rc) {
+__global__ void __launch_bounds__(kXferThreads) k_restrict(MeshDev mc, MeshDev mf, const double* __restrict__ rf,
+                                                           double* __restrict__ rc) {
   using C = XferCfg<PC>;
   constexpr int NC = C::NC, NF = C::NF, PF = C::PF;
   extern __shared__ double sm[];
   double* sf = sm;             // [k][j][i]
   double* t1 = sf + C::NF3;    // [k][j][a]
   double* t2 = t1 + C::R1;     // [k][b][a]
-  double* I = t2 + C::R2;      // [i][a]
-  for (int l = threadIdx.x; l < NF * NC; l += blockDim.x) I[l] = c_I[PC - 1][l];
+  const double* I = c_I[PC - 1];
   const long long e = blockIdx.x;
   int ex, ey, ez;
   ecoords(mf, e, ex, ey, ez);
@@ -128,31 +133,49 @@ __global__ void __launch_bounds__(256) k_restrict(MeshDev mc, MeshDev mf, const 
     sf[l] = v;
   }
   __syncthreads();
-  for (int l = threadIdx.x; l < C::R1; l += blockDim.x) {
-    const int a = l % NC, r = l / NC;     // r = j + NF k
-    double s = 0.0;
+  for (int r = threadIdx.x; r < NF * NF; r += blockDim.x) {   // x: fine line (j, k) -> NC values
+    double L[NF];
 #pragma unroll
-    for (int i = 0; i < NF; ++i) s += I[i * NC + a] * sf[i + NF * r];
-    t1[l] = s;
+    for (int i = 0; i < NF; ++i) L[i] = sf[i + NF * r];
+#pragma unroll
+    for (int a = 0; a < NC; ++a) {
+      double acc = 0.0;
+#pragma unroll
+      for (int i = 0; i < NF; ++i) acc = fma(I[i * NC + a], L[i], acc);
+      t1[a + NC * r] = acc;
+    }
   }
   __syncthreads();
-  for (int l = threadIdx.x; l < C::R2; l += blockDim.x) {
-    const int a = l % NC, b = (l / NC) % NC, k = l / (NC * NC);
-    double s = 0.0;
+  for (int r = threadIdx.x; r < NC * NF; r += blockDim.x) {   // y: line (a, k) over j -> b
+    const int a = r % NC, k = r / NC;
+    double L[NF];
 #pragma unroll
-    for (int j = 0; j < NF; ++j) s += I[j * NC + b] * t1[a + NC * (j + NF * k)];
-    t2[l] = s;
+    for (int j = 0; j < NF; ++j) L[j] = t1[a + NC * (j + NF * k)];
+#pragma unroll
+    for (int b = 0; b < NC; ++b) {
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < NF; ++j) acc = fma(I[j * NC + b], L[j], acc);
+      t2[a + NC * (b + NC * k)] = acc;
+    }
   }
   __syncthreads();
-  for (int l = threadIdx.x; l < C::NC3; l += blockDim.x) {
-    const int a = l % NC, b = (l / NC) % NC, c = l / (NC * NC);
-    const int I0 = ex * PC + a, J0 = ey * PC + b, K0 = ez * PC + c;
-    const bool bnd = I0 == 0 || I0 == mc.Mx - 1 || J0 == 0 || J0 == mc.My - 1 || K0 == 0 || K0 == mc.Mz - 1;
-    if (bnd) continue;
-    double s = 0.0;
+  for (int r = threadIdx.x; r < NC * NC; r += blockDim.x) {   // z: line (a, b) over k -> c, RED
+    const int a = r % NC, b = r / NC;
+    const int I0 = ex * PC + a, J0 = ey * PC + b;
+    if (I0 == 0 || I0 == mc.Mx - 1 || J0 == 0 || J0 == mc.My - 1) continue;
+    double L[NF];
 #pragma unroll
-    for (int k = 0; k < NF; ++k) s += I[k * NC + c] * t2[a + NC * (b + NC * k)];
-    atomicAdd(rc + I0 + (long long)mc.Mx * (J0 + (long long)mc.My * K0), s);
+    for (int k = 0; k < NF; ++k) L[k] = t2[r + NC * NC * k];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const int K0 = ez * PC + c;
+      if (K0 == 0 || K0 == mc.Mz - 1) continue;
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < NF; ++k) acc = fma(I[k * NC + c], L[k], acc);
+      atomicAdd(rc + I0 + (long long)mc.Mx * (J0 + (long long)mc.My * K0), acc);
+    }
   }
 }
 
@@ -181,7 +204,7 @@ static cudaError_t restrict_p(const MeshDev& mc, const MeshDev& mf, const double
   }
   cudaError_t e = cudaMemsetAsync(rc, 0, sizeof(double) * mc.N, s);
   if (e) return e;
-  k_restrict<PC><<<(unsigned)mf.E, 256, C::SMEM_R, s>>>(mc, mf, rf, rc);
+  k_restrict<PC><<<(unsigned)mf.E, kXferThreads, C::SMEM_R, s>>>(mc, mf, rf, rc);
   return cudaGetLastError();
 }
 
