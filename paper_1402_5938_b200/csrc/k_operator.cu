@@ -308,6 +308,9 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 #ifndef SFMG_V4_THR
 #define SFMG_V4_THR 256
 #endif
+#ifndef SFMG_RESIDENT_MAX
+#define SFMG_RESIDENT_MAX 0   // developer knob: cap the persistent apply's blocks per SM
+#endif
 #ifndef SFMG_PF_GS
 #define SFMG_PF_GS 2   // GS: TMA holds group g+1; L2 prefetch of g+2 (3: also g+3)
 #endif
@@ -1199,6 +1202,7 @@ static cudaError_t apply_pd(const MeshDev& m, const double* G, const double* u, 
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
       if (resident < 1) resident = 1;
+      if (SFMG_RESIDENT_MAX > 0 && resident > SFMG_RESIDENT_MAX) resident = SFMG_RESIDENT_MAX;
     }
     const long long groups = (m.E + C::EPB - 1) / C::EPB;
     long long grid = (long long)resident * num_sms;
