@@ -332,6 +332,9 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 #ifndef SFMG_V5_SMEM_BUDGET
 #define SFMG_V5_SMEM_BUDGET 60000
 #endif
+#ifndef SFMG_INIT_EARLY_MAXN
+#define SFMG_INIT_EARLY_MAXN (1ll << 24)   // v init with an early PDL trigger up to this many dofs
+#endif
 #ifndef SFMG_KSTAGE
 #define SFMG_KSTAGE 0
 #endif
@@ -826,7 +829,12 @@ __global__ void __launch_bounds__(256) k_load(MeshDev m, double* f) {
 // v = (I - M) u (bc 0) or 0 (bc 1).  One warp per lattice row (J, K): the only integer divisions
 // are per row, and each lane writes consecutive doubles of the row.
 __global__ void __launch_bounds__(256) k_init(MeshDev m, int bc, const double* __restrict__ u, double bval,
-                                              double* __restrict__ v) {
+                                              double* __restrict__ v, int early) {
+  // early: the grid is one resident wave (8 blocks per SM) and triggers its programmatic dependent
+  // (the persistent apply) at once, so the apply's launch overlaps this kernel; the apply waits
+  // (griddepcontrol.wait) only before its first scatter.  Safe: every init block is already running
+  // when the dependent launches, and an init block never waits on anything.
+  if (early) pdl_trigger();
   const int lane = threadIdx.x & 31;
   const long long rows = (long long)m.My * m.Mz;
   const long long wstride = (long long)gridDim.x * (blockDim.x >> 5);
@@ -841,7 +849,7 @@ __global__ void __launch_bounds__(256) k_init(MeshDev m, int bc, const double* _
       vr[I] = b ? (ur ? ur[I] : bval) : 0.0;
     }
   }
-  pdl_trigger();   // after this block's work (see k_cheb_update)
+  if (!early) pdl_trigger();   // after this block's work (see k_cheb_update)
 }
 
 __global__ void k_cheb_update(MeshDev m, const double* cur, const double* prev, double* out,
@@ -1257,7 +1265,18 @@ cudaError_t launch_load(const MeshDev& m, int rhs_id, double* f, cudaStream_t s)
 }
 
 cudaError_t launch_init(const MeshDev& m, int bc, const double* u, double bval, double* v, cudaStream_t s) {
-  k_init<<<grid_for((long long)m.My * m.Mz * 32, 256), 256, 0, s>>>(m, bc, u, bval, v);
+  int grid = grid_for((long long)m.My * m.Mz * 32, 256);
+  // early trigger only for small vectors: for large ones the init outlasts the apply's first element and
+  // the early-started apply blocks slow it down (config 2 46.3 -> 44.0 us; config 4 2.51 -> 3.21 ms)
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int early = (SFMG_INIT_EARLY_MAXN > 0 && m.N <= SFMG_INIT_EARLY_MAXN) ? 1 : 0;
+  if (early && grid > 8 * sms) grid = 8 * sms;
+  k_init<<<grid, 256, 0, s>>>(m, bc, u, bval, v, early);
   return cudaGetLastError();
 }
 
