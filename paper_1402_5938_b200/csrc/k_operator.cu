@@ -332,6 +332,9 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 #ifndef SFMG_V5_SMEM_BUDGET
 #define SFMG_V5_SMEM_BUDGET 60000
 #endif
+#ifndef SFMG_UPD_EARLY_MAXN
+#define SFMG_UPD_EARLY_MAXN (1ll << 24)   // Chebyshev update with an early PDL trigger up to this many dofs
+#endif
 #ifndef SFMG_INIT_EARLY_MAXN
 #define SFMG_INIT_EARLY_MAXN (1ll << 24)   // v init with an early PDL trigger up to this many dofs
 #endif
@@ -854,7 +857,8 @@ __global__ void __launch_bounds__(256) k_init(MeshDev m, int bc, const double* _
 
 __global__ void k_cheb_update(MeshDev m, const double* cur, const double* prev, double* out,
                               const double* __restrict__ b, double* y, const double* __restrict__ dinv,
-                              double c1, double c2) {
+                              double c1, double c2, int early) {
+  if (early) pdl_trigger();   // one resident wave: see k_init
   for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < m.N; g += (long long)gridDim.x * blockDim.x) {
     const double xc = cur[g];
     const double xp = (c1 != 0.0) ? prev[g] : 0.0;
@@ -862,8 +866,8 @@ __global__ void k_cheb_update(MeshDev m, const double* cur, const double* prev, 
     out[g] = xn;
     y[g] = lattice_boundary(m, g) ? xn : 0.0;
   }
-  pdl_trigger();   // after this block's work: every block of this grid is then resident or done, so
-                   // the dependent persistent apply can never starve it of SM resources
+  if (!early) pdl_trigger();   // after this block's work: every block of this grid is then resident or
+                               // done, so the dependent persistent apply can never starve it of SM resources
 }
 
 __global__ void k_export_maps(MeshDev m, int32_t* l2g, uint8_t* mask, uint8_t* col) {
@@ -1283,7 +1287,18 @@ cudaError_t launch_init(const MeshDev& m, int bc, const double* u, double bval, 
 cudaError_t launch_cheb_update(const MeshDev& m, const double* cur, const double* prev, double* out,
                                const double* b, double* y, const double* dinv, double c1, double c2,
                                cudaStream_t s) {
-  k_cheb_update<<<grid_for(m.N, 256), 256, 0, s>>>(m, cur, prev, out, b, y, dinv, c1, c2);
+  int grid = grid_for(m.N, 256);
+  static int resident = 0;
+  if (!resident) {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_cheb_update, 256, 0);
+    resident = (per > 0 ? per : 1) * sms;
+  }
+  const int early = (SFMG_UPD_EARLY_MAXN > 0 && m.N <= SFMG_UPD_EARLY_MAXN) ? 1 : 0;
+  if (early && grid > resident) grid = resident;
+  k_cheb_update<<<grid, 256, 0, s>>>(m, cur, prev, out, b, y, dinv, c1, c2, early);
   return cudaGetLastError();
 }
 
