@@ -332,6 +332,9 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 #ifndef SFMG_V5_SMEM_BUDGET
 #define SFMG_V5_SMEM_BUDGET 60000
 #endif
+#ifndef SFMG_APPLY_TRIGGER
+#define SFMG_APPLY_TRIGGER 1   // persistent apply triggers its dependent at its last group; update is PDL
+#endif
 #ifndef SFMG_UPD_EARLY_MAXN
 #define SFMG_UPD_EARLY_MAXN (1ll << 24)   // Chebyshev update with an early PDL trigger up to this many dofs
 #endif
@@ -454,6 +457,9 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
   unsigned phase = 0;
   for (; grp < ngroups; grp += gstride) {
     constexpr int zero = 0;
+    // last group of this block: let a programmatic dependent (the Chebyshev update) launch now; it
+    // waits (griddepcontrol.wait) for this grid's completion before reading v
+    if (SFMG_APPLY_TRIGGER && grp + gstride >= ngroups) pdl_trigger();
     const long long e = grp * C::EPB + le;
     const bool act = e < m.E;
     int ex = 0, ey = 0, ez = 0;
@@ -859,6 +865,7 @@ __global__ void k_cheb_update(MeshDev m, const double* cur, const double* prev, 
                               const double* __restrict__ b, double* y, const double* __restrict__ dinv,
                               double c1, double c2, int early) {
   if (early) pdl_trigger();   // one resident wave: see k_init
+  if (SFMG_APPLY_TRIGGER) pdl_wait();   // launched as the apply's programmatic dependent
   for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < m.N; g += (long long)gridDim.x * blockDim.x) {
     const double xc = cur[g];
     const double xp = (c1 != 0.0) ? prev[g] : 0.0;
@@ -1298,6 +1305,8 @@ cudaError_t launch_cheb_update(const MeshDev& m, const double* cur, const double
   }
   const int early = (SFMG_UPD_EARLY_MAXN > 0 && m.N <= SFMG_UPD_EARLY_MAXN) ? 1 : 0;
   if (early && grid > resident) grid = resident;
+  if (SFMG_APPLY_TRIGGER)
+    return launch_pdl(k_cheb_update, (unsigned)grid, 256u, 0, s, m, cur, prev, out, b, y, dinv, c1, c2, early);
   k_cheb_update<<<grid, 256, 0, s>>>(m, cur, prev, out, b, y, dinv, c1, c2, early);
   return cudaGetLastError();
 }
