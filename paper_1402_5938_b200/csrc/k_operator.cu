@@ -11,6 +11,7 @@
 // is unrolled, every D index is a compile-time constant, and DFMA takes D as a constant-bank
 // operand (no load instruction).
 #include <cstdio>
+#include <cstdlib>
 
 #include "k_common.cuh"
 
@@ -335,12 +336,18 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 #ifndef SFMG_APPLY_TRIGGER
 #define SFMG_APPLY_TRIGGER 1   // persistent apply triggers its dependent at its last group; update is PDL
 #endif
-#ifndef SFMG_UPD_EARLY_MAXN
-#define SFMG_UPD_EARLY_MAXN (1ll << 24)   // Chebyshev update with an early PDL trigger up to this many dofs
-#endif
-#ifndef SFMG_INIT_EARLY_MAXN
-#define SFMG_INIT_EARLY_MAXN (1ll << 24)   // v init with an early PDL trigger up to this many dofs
-#endif
+// Early programmatic-dependent triggers (v init, Chebyshev update, apply -> update) are used for
+// vectors of at most this many dofs; SFMG_EARLY_MAXN in the environment overrides it (0: never; the
+// tests run both paths).
+constexpr long long kEarlyMaxN = 1ll << 24;
+static bool early_pdl(const MeshDev& m) {
+  static long long thr = -1;
+  if (thr < 0) {
+    const char* e = getenv("SFMG_EARLY_MAXN");
+    thr = e ? atoll(e) : kEarlyMaxN;
+  }
+  return m.N <= thr;
+}
 #ifndef SFMG_KSTAGE
 #define SFMG_KSTAGE 0
 #endif
@@ -460,7 +467,7 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
     // last group of this block: let a programmatic dependent (the Chebyshev update) launch now; it
     // waits (griddepcontrol.wait) for this grid's completion before reading v.  Small vectors only
     // (config 4 measured 2.51 -> 2.61 ms with it)
-    if (SFMG_APPLY_TRIGGER && m.N <= SFMG_UPD_EARLY_MAXN && grp + gstride >= ngroups) pdl_trigger();
+    if (SFMG_APPLY_TRIGGER && m.pdl_early && grp + gstride >= ngroups) pdl_trigger();
     const long long e = grp * C::EPB + le;
     const bool act = e < m.E;
     int ex = 0, ey = 0, ez = 0;
@@ -1227,7 +1234,9 @@ static cudaError_t apply_pd(const MeshDev& m, const double* G, const double* u, 
     const long long groups = (m.E + C::EPB - 1) / C::EPB;
     long long grid = (long long)resident * num_sms;
     if (grid > groups) grid = groups;
-    return launch_pdl(k_apply_v4<P, DIR, GS>, (unsigned)grid, (unsigned)C::THREADS, C::SMEM, s, m, G, u, v, groups,
+    MeshDev mm = m;
+    mm.pdl_early = early_pdl(m) ? 1 : 0;
+    return launch_pdl(k_apply_v4<P, DIR, GS>, (unsigned)grid, (unsigned)C::THREADS, C::SMEM, s, mm, G, u, v, groups,
                       wait_mode, write_bnd);
   }
 }
@@ -1286,7 +1295,7 @@ cudaError_t launch_init(const MeshDev& m, int bc, const double* u, double bval, 
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  const int early = (SFMG_INIT_EARLY_MAXN > 0 && m.N <= SFMG_INIT_EARLY_MAXN) ? 1 : 0;
+  const int early = early_pdl(m) ? 1 : 0;
   if (early && grid > 8 * sms) grid = 8 * sms;
   k_init<<<grid, 256, 0, s>>>(m, bc, u, bval, v, early);
   return cudaGetLastError();
@@ -1304,7 +1313,7 @@ cudaError_t launch_cheb_update(const MeshDev& m, const double* cur, const double
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_cheb_update, 256, 0);
     resident = (per > 0 ? per : 1) * sms;
   }
-  const int early = (SFMG_UPD_EARLY_MAXN > 0 && m.N <= SFMG_UPD_EARLY_MAXN) ? 1 : 0;
+  const int early = early_pdl(m) ? 1 : 0;
   if (early && grid > resident) grid = resident;
   if (SFMG_APPLY_TRIGGER)
     return launch_pdl(k_cheb_update, (unsigned)grid, 256u, 0, s, m, cur, prev, out, b, y, dinv, c1, c2, early);

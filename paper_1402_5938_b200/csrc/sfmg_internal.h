@@ -28,6 +28,7 @@ struct MeshDev {
   // apply and init kernels only.
   int Kb0, Kb1;
   int dim = 3;             // 3 hexahedra; 2 quadrilaterals (NEXT-2: nez = 1, Mz = 1, Kb0 = Kb1 = -1)
+  int pdl_early = 0;       // set per launch: early programmatic-dependent triggers (small vectors)
 };
 
 // Device reduction scratch: partials[kRedBlocks][kRedSlots], scalars[32], counter.

@@ -1,0 +1,57 @@
+"""Both launch schedules of the apply / Chebyshev kernels against the oracle (run with -m gpu).
+
+For vectors of <= 2^24 dofs the v init, the Chebyshev update and the persistent apply trigger their
+programmatic dependents early ("Launch overlap"); larger vectors take the
+completion-ordered path.  The in-process GPU tests only reach the early path (their meshes are small),
+so this test re-runs an apply and a Chebyshev application in a subprocess with SFMG_EARLY_MAXN=0, which
+forces the completion-ordered path, and checks both against the oracle with the section-2 bars.
+"""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+SCRIPT = r"""
+import json, sys
+import numpy as np
+sys.path.insert(0, %(root)r)
+import torch
+import oracle
+from paper_1402_5938_b200 import inputs, sfmg
+oracle.build()
+out = {}
+for p in (4, 8, 16):
+    d = inputs.problem(2, p, ney=2, nez=2, warp=1, amp=0.1, coeff=1, c0=1.0, c1=3.0)
+    g = sfmg.Level(sfmg.Problem.from_dict(d))
+    o = oracle.Level(d["nex"], d["ney"], d["nez"], p, 1, 0.1, 1, 1.0, 3.0, eager=True, tier=3, geom_tier=2)
+    u = inputs.uniform_pm1(5, o.N)
+    vo = o.apply(u, 0, 3)
+    v = torch.empty(o.N, dtype=torch.float64, device="cuda")
+    g.apply(torch.from_numpy(u).cuda(), v)
+    ea = float(np.abs(v.cpu().numpy() - vo).max() / np.abs(vo).max())
+    lam = o.lambda_max(10, 12345)
+    b = inputs.uniform_pm1(6, o.N)
+    xo = o.cheb(b, u, 4, 0.1 * lam, 1.1 * lam)
+    xg = g.cheb(torch.from_numpy(b).cuda(), torch.from_numpy(u.copy()).cuda(), 4, 0.1 * lam, 1.1 * lam).cpu().numpy()
+    ec = float(np.abs(xg - xo).max() / np.abs(xo).max())
+    out[p] = [ea, ec]
+print(json.dumps(out))
+"""
+
+
+@pytest.mark.parametrize("maxn", ["0", str(1 << 24)], ids=["completion_ordered", "early_triggers"])
+def test_launch_schedules_match_oracle(maxn):
+    env = dict(os.environ, SFMG_EARLY_MAXN=maxn)
+    r = subprocess.run([sys.executable, "-c", SCRIPT % {"root": ROOT}], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    res = json.loads(r.stdout.strip().splitlines()[-1])
+    for p, (ea, ec) in res.items():
+        assert ea <= 1e-11, (p, ea)   # ||A u||_inf normaliser (R19, stricter than ||A|| ||u||)
+        assert ec <= 1e-11, (p, ec)   # R18
