@@ -348,6 +348,9 @@ static bool early_pdl(const MeshDev& m) {
   }
   return m.N <= thr;
 }
+#ifndef SFMG_TRANSPOSED_Y
+#define SFMG_TRANSPOSED_Y 1
+#endif
 #ifndef SFMG_KSTAGE
 #define SFMG_KSTAGE 0
 #endif
@@ -381,6 +384,11 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
   // during the whole element (measured: p = 16 -2.5 %, p <= 8 within noise)
   // (p >= 12: off; the u columns are L2-prefetched instead, which frees 2n registers: p = 16 -2 %)
   constexpr bool EARLY = (P >= 12) ? (SFMG_EARLY > 1) : (SFMG_EARLY > 0);
+  // TR: the y-direction data live in a transposed array (index j + n i + n^2 k), so the y-line passes
+  // read and write it with the x-lines' conflict-free stride; s0 holds u -> g0 -> w0 -> X (natural layout,
+  // x-lines in place), su holds u -> g1 -> w1 -> Y (transposed, y-lines in place), and the z-line pass
+  // adds X + Y + Z.  Removes the 2-way bank conflicts of natural-layout y-lines at p = 8.
+  constexpr bool TR = SFMG_TRANSPOSED_Y && GS && P == 8;   // measured: p = 8 step -2 %, p = 4 +1 %
   extern __shared__ __align__(128) double smem[];
   double* sG = smem;                                   // [EPB][k][6][n^2] (GS)
   const int le = threadIdx.x / N2;
@@ -489,18 +497,26 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
 #pragma unroll
         for (int c = 0; c < 6; ++c) gb[kk][c] = __ldcs(Gg + gofs<N>(c, 0, KST + kk));
     }
+    if (TR) {
 #pragma unroll
-    for (int k = 0; k < N; ++k) su[t + N2 * k] = ru[k];
+      for (int k = 0; k < N; ++k) {
+        s0[t + N2 * k] = ru[k];
+        su[t1 + N * t0 + N2 * k] = ru[k];
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < N; ++k) su[t + N2 * k] = ru[k];
+    }
     double rn[N];
     if (EARLY && grp + gstride < ngroups) {   // next group's u column, in flight during the whole element
       load_column(grp + gstride, rn);
       if (grp + 2 * gstride < ngroups) prefetch_column(grp + 2 * gstride);
     }
     __syncthreads();
-    {  // P1: g0 on x-line (j=t0, k=t1) -> s0
+    {  // P1: g0 on x-line (j=t0, k=t1) -> s0 (TR: in place)
       double L[N];
 #pragma unroll
-      for (int mm = 0; mm < N; ++mm) L[mm] = su[mm + N * t0 + N2 * t1];
+      for (int mm = 0; mm < N; ++mm) L[mm] = (TR ? s0 : su)[mm + N * t0 + N2 * t1];
       if constexpr (EO) {
         double o[N];
         eo_line<P, 0>(L, o);
@@ -518,21 +534,24 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
     }
     __syncthreads();
     {  // P2: g1 on y-line (i=t0, k=t1), in place in su
+      // y-line element j of line (i, k): natural su[i + n j + n^2 k], transposed su[j + n i + n^2 k]
+      const int yb = TR ? N * t0 + N2 * t1 : t0 + N2 * t1;
+      constexpr int ys = TR ? 1 : N;
       double L[N];
 #pragma unroll
-      for (int mm = 0; mm < N; ++mm) L[mm] = su[t0 + N * mm + N2 * t1];
+      for (int mm = 0; mm < N; ++mm) L[mm] = su[yb + ys * mm];
       if constexpr (EO) {
         double o[N];
         eo_line<P, 1>(L, o);
 #pragma unroll
-        for (int j = 0; j < N; ++j) su[t0 + N * j + N2 * t1] = o[j];
+        for (int j = 0; j < N; ++j) su[yb + ys * j] = o[j];
       } else {
 #pragma unroll
         for (int j = 0; j < N; ++j) {
           double s = 0.0;
 #pragma unroll
           for (int mm = 0; mm < N; ++mm) s = fma(dmat<P>(1, j * N + mm + zero), L[mm], s);
-          su[t0 + N * j + N2 * t1] = s;
+          su[yb + ys * j] = s;
         }
       }
     }
@@ -572,9 +591,10 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
           G11 = gb[kr % RG][3]; G12 = gb[kr % RG][4]; G22 = gb[kr % RG][5];
         }
         const int idx = t + N2 * k;
-        const double g0 = s0[idx], g1 = su[idx], g2 = g2a[k];
+        const int idy = TR ? t1 + N * t0 + N2 * k : idx;   // (t0, t1, k) in su's layout
+        const double g0 = s0[idx], g1 = su[idy], g2 = g2a[k];
         s0[idx] = G00 * g0 + G01 * g1 + G02 * g2;
-        su[idx] = G01 * g0 + G11 * g1 + G12 * g2;
+        su[idy] = G01 * g0 + G11 * g1 + G12 * g2;
         g2a[k] = G02 * g0 + G12 * g1 + G22 * g2;
       }
       if constexpr (EO) {
@@ -629,22 +649,24 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
       }
     }
     __syncthreads();
-    {  // P5: su = D^T w1 + v0 on y-line (i=t0, k=t1)
+    {  // P5: su = D^T w1 + v0 on y-line (i=t0, k=t1) (TR: su = Y in place; v0 is added in P6)
+      const int yb = TR ? N * t0 + N2 * t1 : t0 + N2 * t1;
+      constexpr int ys = TR ? 1 : N;
       double L[N];
 #pragma unroll
-      for (int mm = 0; mm < N; ++mm) L[mm] = su[t0 + N * mm + N2 * t1];
+      for (int mm = 0; mm < N; ++mm) L[mm] = su[yb + ys * mm];
       if constexpr (EO) {
         double o[N];
         eo_line<P, 5>(L, o);
 #pragma unroll
-        for (int b = 0; b < N; ++b) su[t0 + N * b + N2 * t1] = o[b] + s0[t0 + N * b + N2 * t1];
+        for (int b = 0; b < N; ++b) su[yb + ys * b] = TR ? o[b] : o[b] + s0[t0 + N * b + N2 * t1];
       } else {
 #pragma unroll
         for (int b = 0; b < N; ++b) {
-          double s = s0[t0 + N * b + N2 * t1];
+          double s = TR ? 0.0 : s0[t0 + N * b + N2 * t1];
 #pragma unroll
           for (int mm = 0; mm < N; ++mm) s = fma(dmat<P>(4, mm * N + b + zero), L[mm], s);
-          su[t0 + N * b + N2 * t1] = s;
+          su[yb + ys * b] = s;
         }
       }
     }
@@ -659,7 +681,8 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
       for (int c = 0; c < N; ++c) {
         bool bnd = false;
         if (DIR) { const int K = ez * P + c; bnd = bxy || K == m.Kb0 || K == m.Kb1; }
-        if (!bnd) atomicAdd(v + gcol + sxy * c, su[t + N2 * c] + vz[c]);
+        const double xy = TR ? s0[t + N2 * c] + su[t1 + N * t0 + N2 * c] : su[t + N2 * c];
+        if (!bnd) atomicAdd(v + gcol + sxy * c, xy + vz[c]);
         else if (write_bnd && own_xy && (c > 0 || ez == 0)) v[gcol + sxy * c] = u[gcol + sxy * c];  // (I-M) u
       }
     }
