@@ -294,47 +294,56 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // GS = true : the group's factors are staged in smem by one TMA bulk copy (p <= 8 fits).
-// GS = false: P3 reads the factors straight from L2 into registers (three k-slices in flight);
-//             the whole next-but-one element is TMA-prefetched into L2 (p >= 9: G of one element is
-//             up to 236 KB and cannot be staged).
+// GS = false: P3 reads the factors straight from L2 into registers through a k-slice ring, with the
+//             next element TMA-prefetched into L2 (p >= 9: G of one element is up to 236 KB and cannot
+//             be staged).
+//
+// Compile-time knobs.  The defaults are the measured choices; the alternatives are kept so that the
+// A/B builds of tools/build_variant.py can re-measure them (profiles/r01_experiments.md has the numbers).
 #ifndef SFMG_PF_AHEAD
-#define SFMG_PF_AHEAD 1
+#define SFMG_PF_AHEAD 1        // !GS: L2 prefetch distance in groups (2 overflows L2 at p = 16)
 #endif
 #ifndef SFMG_RING
-#define SFMG_RING 5
+#define SFMG_RING 5            // !GS: register ring depth in k-slices (loads RING - 1 slices ahead)
 #endif
 #ifndef SFMG_V4_SMEM
-#define SFMG_V4_SMEM 52000   // smem budget per block that sets the elements per block (p <= 8)
+#define SFMG_V4_SMEM 52000     // smem budget per block that sets the elements per block (p <= 8)
 #endif
 #ifndef SFMG_V4_THR
-#define SFMG_V4_THR 256
+#define SFMG_V4_THR 256        // thread budget per block that sets the elements per block
 #endif
 #ifndef SFMG_RESIDENT_MAX
-#define SFMG_RESIDENT_MAX 0   // developer knob: cap the persistent apply's blocks per SM
+#define SFMG_RESIDENT_MAX 0    // > 0: cap the persistent apply's blocks per SM (occupancy sweeps)
 #endif
 #ifndef SFMG_PF_GS
-#define SFMG_PF_GS 2   // GS: TMA holds group g+1; L2 prefetch of g+2 (3: also g+3)
+#define SFMG_PF_GS 2           // GS, long grids: L2 prefetch of group g+2 (3: also g+3)
 #endif
 #ifndef SFMG_PF_START
-#define SFMG_PF_START 0   // 0: no L2 prefetch burst at kernel start (steady-state prefetches only)
+#define SFMG_PF_START 0        // 1: L2 prefetch burst at kernel start as well (slower at config 2)
 #endif
 #ifndef SFMG_PF_TOP
-#define SFMG_PF_TOP 0
+#define SFMG_PF_TOP 0          // !GS: 1 = prefetch the next element at the element top (L2 overflow)
 #endif
 #ifndef SFMG_MINB_HI
-#define SFMG_MINB_HI 1
+#define SFMG_MINB_HI 1         // p >= 12: blocks per SM requested from ptxas (2 spills)
 #endif
 #ifndef SFMG_EARLY
-#define SFMG_EARLY 1
+#define SFMG_EARLY 1           // register prefetch of the next u column (p <= 11; 2: also p >= 12)
 #endif
 #ifndef SFMG_V5
-#define SFMG_V5 0            // 1: even p >= 4 through k_apply_v5.cuh (two threads per line; measured slower, kept off)
+#define SFMG_V5 0              // 1: even p >= 4 through k_apply_v5.cuh (two threads per line; slower)
 #endif
 #ifndef SFMG_V5_SMEM_BUDGET
 #define SFMG_V5_SMEM_BUDGET 60000
 #endif
 #ifndef SFMG_APPLY_TRIGGER
 #define SFMG_APPLY_TRIGGER 1   // persistent apply triggers its dependent at its last group; update is PDL
+#endif
+#ifndef SFMG_TRANSPOSED_Y
+#define SFMG_TRANSPOSED_Y 1    // p = 8: y-direction data in a transposed smem array (fewer bank conflicts)
+#endif
+#ifndef SFMG_KSTAGE
+#define SFMG_KSTAGE 0          // !GS, one element per block: first k-slices TMA-staged in free smem
 #endif
 // Early programmatic-dependent triggers (v init, Chebyshev update, apply -> update) are used for
 // vectors of at most this many dofs; SFMG_EARLY_MAXN in the environment overrides it (0: never; the
@@ -348,12 +357,6 @@ static bool early_pdl(const MeshDev& m) {
   }
   return m.N <= thr;
 }
-#ifndef SFMG_TRANSPOSED_Y
-#define SFMG_TRANSPOSED_Y 1
-#endif
-#ifndef SFMG_KSTAGE
-#define SFMG_KSTAGE 0
-#endif
 
 template <int P, bool GS>
 struct V4Cfg {
