@@ -26,7 +26,7 @@ import oracle
 from paper_1402_5938_b200 import inputs, sfmg
 oracle.build()
 out = {}
-for p in (4, 8, 16):
+for p in (3, 4, 5, 8, 9, 12, 16):
     d = inputs.problem(2, p, ney=2, nez=2, warp=1, amp=0.1, coeff=1, c0=1.0, c1=3.0)
     g = sfmg.Level(sfmg.Problem.from_dict(d))
     o = oracle.Level(d["nex"], d["ney"], d["nez"], p, 1, 0.1, 1, 1.0, 3.0, eager=True, tier=3, geom_tier=2)
