@@ -276,6 +276,18 @@ struct GaussCfg {
   static constexpr size_t SMEM = sizeof(double) * 3 * N3 * EPB;
 };
 
+// L2 prefetch (TMA bulk, evict-first policy: the factors are read once) of one group's factors and
+// a group's u columns, issued one group ahead so that the pointwise pass and the gather of the next
+// group hit L2 (the collocated kernel's scheme, k_operator.cu).
+__device__ __forceinline__ void gauss_prefetch_l2(const void* src, unsigned bytes) {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  for (unsigned o = 0; o < bytes; o += 65536u)
+    asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"((const char*)src + o),
+                 "r"(bytes - o < 65536u ? bytes - o : 65536u), "l"(pol)
+                 : "memory");
+}
+
 // Block = EPB elements x n^2 threads; thread (t0, t1) owns one line per pass (see file header).
 template <int P, bool DIR>
 __global__ void __launch_bounds__(GaussCfg<P>::THREADS) k_apply_gauss(MeshDev m, const double* __restrict__ G,
@@ -290,11 +302,31 @@ __global__ void __launch_bounds__(GaussCfg<P>::THREADS) k_apply_gauss(MeshDev m,
   double* Cc = Bb + N3;
   const long long sxy = (long long)m.Mx * m.My;
   const long long ngroups = (m.E + C::EPB - 1) / C::EPB;
+  constexpr bool PFG = !GLayout<P>::kTPE;   // slice-major factors: a group is one contiguous block
+  auto group_bytes = [&](long long g) -> unsigned {
+    long long nel = m.E - g * C::EPB;
+    if (nel > C::EPB) nel = C::EPB;
+    return (unsigned)(nel * 6 * N3 * sizeof(double));
+  };
+  if (PFG && threadIdx.x == 0 && blockIdx.x < ngroups)
+    gauss_prefetch_l2(G + (long long)blockIdx.x * C::EPB * 6 * N3, group_bytes(blockIdx.x));
   for (long long grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
     const long long e = grp * C::EPB + le;
     const bool act = e < m.E;
     int ex = 0, ey = 0, ez = 0;
     if (act) elem_coords(m, e, ex, ey, ez);
+    const long long nx = grp + gridDim.x;
+    if (PFG && nx < ngroups) {   // next group: factors (thread 0) and this thread's u column
+      if (threadIdx.x == 0) gauss_prefetch_l2(G + nx * C::EPB * 6 * N3, group_bytes(nx));
+      const long long en = nx * C::EPB + le;
+      if (en < m.E) {
+        int qx, qy, qz;
+        elem_coords(m, en, qx, qy, qz);
+        const double* pu = u + (long long)(qx * P + t0) + (long long)m.Mx * (qy * P + t1) + sxy * (long long)(qz * P);
+#pragma unroll
+        for (int c = 0; c < N; ++c) asm volatile("prefetch.global.L2 [%0];" ::"l"(pu + sxy * c));
+      }
+    }
     __syncthreads();
     {  // gather: nodal column (a = t0, b = t1), masked (R4)
       const int I = ex * P + t0, J = ey * P + t1;
@@ -359,9 +391,9 @@ __global__ void __launch_bounds__(GaussCfg<P>::THREADS) k_apply_gauss(MeshDev m,
 #pragma unroll
       for (int k = 0; k < N; ++k) {
         const int idx = t0 + N * t1 + N2 * k, ij = t0 + N * t1;
-        const double G00 = __ldg(G + GLayout<P>::off(eg, 0, ij, k)), G01 = __ldg(G + GLayout<P>::off(eg, 1, ij, k));
-        const double G02 = __ldg(G + GLayout<P>::off(eg, 2, ij, k)), G11 = __ldg(G + GLayout<P>::off(eg, 3, ij, k));
-        const double G12 = __ldg(G + GLayout<P>::off(eg, 4, ij, k)), G22 = __ldg(G + GLayout<P>::off(eg, 5, ij, k));
+        const double G00 = __ldcs(G + GLayout<P>::off(eg, 0, ij, k)), G01 = __ldcs(G + GLayout<P>::off(eg, 1, ij, k));
+        const double G02 = __ldcs(G + GLayout<P>::off(eg, 2, ij, k)), G11 = __ldcs(G + GLayout<P>::off(eg, 3, ij, k));
+        const double G12 = __ldcs(G + GLayout<P>::off(eg, 4, ij, k)), G22 = __ldcs(G + GLayout<P>::off(eg, 5, ij, k));
         const double a0 = A[idx], a1 = Bb[idx], a2 = g2[k];
         A[idx] = G00 * a0 + G01 * a1 + G02 * a2;
         Bb[idx] = G01 * a0 + G11 * a1 + G12 * a2;
