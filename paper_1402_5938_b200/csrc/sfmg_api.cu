@@ -331,6 +331,13 @@ static void free_prof(sfmg_level_s* lv) {
   if (lv->hp_h2d) cudaStreamDestroy(lv->hp_h2d);
   if (lv->hp_d2h) cudaStreamDestroy(lv->hp_d2h);
   lv->hp_h2d = lv->hp_d2h = nullptr;
+  if (lv->cgc_exec) cudaGraphExecDestroy(lv->cgc_exec);
+  for (cudaEvent_t& ev : lv->cgc_ev)
+    if (ev) cudaEventDestroy(ev), ev = nullptr;
+  if (lv->cgc_s) cudaStreamDestroy(lv->cgc_s);
+  lv->cgc_exec = nullptr;
+  lv->cgc_s = nullptr;
+  lv->cgc_x = lv->cgc_r = nullptr;
 }
 
 sfmg_status sfmg_level_destroy(sfmg_level lv) {
@@ -811,11 +818,53 @@ static cudaError_t coarse_cg_any(sfmg_level_s* lv, const double* b, double* x, d
   if ((e = launch_dot(lv->red, b, b, N, kCgcBB, s))) return e;
   if ((e = launch_cgc_start(lv->red, s))) return e;
   double flag = 0.0;
-  for (int it = 0; it < maxit; it += kCgcBatch) {
+  auto batch = [&](cudaStream_t st) -> cudaError_t {
+    cudaError_t be;
     for (int k = 0; k < kCgcBatch; ++k) {
-      if ((e = op_apply(lv, 0, p, q, s))) return e;
-      if ((e = launch_dot(lv->red, p, q, N, kCgcPQ, s))) return e;
-      if ((e = launch_cgc_iter_tail(lv->red, x, r, p, q, N, rtol, maxit, s))) return e;
+      if ((be = op_apply(lv, 0, p, q, st))) return be;
+      if ((be = launch_dot(lv->red, p, q, N, kCgcPQ, st))) return be;
+      if ((be = launch_cgc_iter_tail(lv->red, x, r, p, q, N, rtol, maxit, st))) return be;
+    }
+    return cudaSuccess;
+  };
+  // a batch is ~6 small kernels per iteration on a small level: replay it as one captured graph on the
+  // level's own stream (the caller's stream may be the legacy one, which cannot be captured)
+  static const bool no_graph = getenv("SFMG_NO_GRAPH") && getenv("SFMG_NO_GRAPH")[0] == '1';
+  bool use_graph = !no_graph && !lv->prof;
+  if (use_graph && (!lv->cgc_exec || lv->cgc_x != x || lv->cgc_r != r || lv->cgc_rtol != rtol ||
+                    lv->cgc_maxit != maxit)) {
+    if (!lv->cgc_s && (e = cudaStreamCreateWithFlags(&lv->cgc_s, cudaStreamNonBlocking))) return e;
+    for (cudaEvent_t& ev : lv->cgc_ev)
+      if (!ev && (e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming))) return e;
+    if (lv->cgc_exec) {
+      cudaGraphExecDestroy(lv->cgc_exec);
+      lv->cgc_exec = nullptr;
+    }
+    cudaGraph_t g = nullptr;
+    if ((e = cudaStreamBeginCapture(lv->cgc_s, cudaStreamCaptureModeThreadLocal))) return e;
+    const cudaError_t ce = batch(lv->cgc_s);
+    const cudaError_t ee = cudaStreamEndCapture(lv->cgc_s, &g);
+    if (ce || ee) {
+      if (g) cudaGraphDestroy(g);
+      return ce ? ce : ee;
+    }
+    e = cudaGraphInstantiate(&lv->cgc_exec, g, 0);
+    cudaGraphDestroy(g);
+    if (e) return e;
+    lv->cgc_x = x;
+    lv->cgc_r = r;
+    lv->cgc_rtol = rtol;
+    lv->cgc_maxit = maxit;
+  }
+  for (int it = 0; it < maxit; it += kCgcBatch) {
+    if (use_graph) {
+      if ((e = cudaEventRecord(lv->cgc_ev[0], s))) return e;
+      if ((e = cudaStreamWaitEvent(lv->cgc_s, lv->cgc_ev[0], 0))) return e;
+      if ((e = cudaGraphLaunch(lv->cgc_exec, lv->cgc_s))) return e;
+      if ((e = cudaEventRecord(lv->cgc_ev[1], lv->cgc_s))) return e;
+      if ((e = cudaStreamWaitEvent(s, lv->cgc_ev[1], 0))) return e;
+    } else if ((e = batch(s))) {
+      return e;
     }
     if ((e = cudaMemcpyAsync(&flag, lv->red.scalars + kCgcFlag, sizeof(double), cudaMemcpyDeviceToHost, s))) return e;
     if ((e = cudaStreamSynchronize(s))) return e;

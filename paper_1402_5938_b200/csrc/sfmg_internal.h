@@ -79,6 +79,15 @@ struct sfmg_level_s {
   cudaStream_t hp_h2d = nullptr, hp_d2h = nullptr;
   int hp_slabs = 0;                 // 0: automatic slab count, else forced (sfmg_host_pipeline)
   std::vector<cudaEvent_t> hp_ev;   // [0] start, then [1 + 3c + {0,1,2}] = H2D / compute / D2H done
+  // host-polled coarse CG (sfmg_api.cu coarse_cg_any): one batch of iterations captured as a CUDA graph
+  // on the level's own stream, for one (x, r) pair
+  cudaStream_t cgc_s = nullptr;
+  cudaEvent_t cgc_ev[2] = {nullptr, nullptr};
+  cudaGraphExec_t cgc_exec = nullptr;
+  const double* cgc_x = nullptr;
+  const double* cgc_r = nullptr;
+  double cgc_rtol = 0.0;
+  int cgc_maxit = 0;
 };
 
 struct sfmg_hier_s {
