@@ -342,6 +342,9 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 #ifndef SFMG_TRANSPOSED_Y
 #define SFMG_TRANSPOSED_Y 1    // p = 8: y-direction data in a transposed smem array (fewer bank conflicts)
 #endif
+#ifndef SFMG_IPS
+#define SFMG_IPS 1             // plain stores for element-interior nodes when N > 2^24 (see k_apply_v4)
+#endif
 #ifndef SFMG_KSTAGE
 #define SFMG_KSTAGE 0          // !GS, one element per block: first k-slices TMA-staged in free smem
 #endif
@@ -376,7 +379,11 @@ struct V4Cfg {
   static constexpr int MINB = GS ? MINB_SMEM : (P >= 12 ? SFMG_MINB_HI : 2);
 };
 
-template <int P, bool DIR, bool GS>
+// IPS: element-interior nodes (one owner element) take a plain store instead of an fp64 RED (v must be
+// zero there beforehand, as the init kernels leave it).  Used for vectors larger than L2 (N > 2^24)
+// right after the v init, where a RED into a line that the init already evicted costs an HBM read; for
+// L2-resident vectors the REDs are cheaper (config 2 measured slower with plain stores).
+template <int P, bool DIR, bool GS, bool IPS = false>
 __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
     k_apply_v4(MeshDev m, const double* __restrict__ G, const double* __restrict__ u, double* __restrict__ v,
                long long ngroups, int wait_mode, int write_bnd) {
@@ -685,7 +692,8 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
         bool bnd = false;
         if (DIR) { const int K = ez * P + c; bnd = bxy || K == m.Kb0 || K == m.Kb1; }
         const double xy = TR ? s0[t + N2 * c] + su[t1 + N * t0 + N2 * c] : su[t + N2 * c];
-        if (!bnd) atomicAdd(v + gcol + sxy * c, xy + vz[c]);
+        if (IPS && t0 > 0 && t0 < P && t1 > 0 && t1 < P && c > 0 && c < P) v[gcol + sxy * c] = xy + vz[c];
+        else if (!bnd) atomicAdd(v + gcol + sxy * c, xy + vz[c]);
         else if (write_bnd && own_xy && (c > 0 || ez == 0)) v[gcol + sxy * c] = u[gcol + sxy * c];  // (I-M) u
       }
     }
@@ -1262,6 +1270,18 @@ static cudaError_t apply_pd(const MeshDev& m, const double* G, const double* u, 
     if (grid > groups) grid = groups;
     MeshDev mm = m;
     mm.pdl_early = early_pdl(m) ? 1 : 0;
+    if (SFMG_IPS && !mm.pdl_early && wait_mode == 1) {   // after the v init (measured: config 4 apply -5 %;
+                                                           // after a Chebyshev update it costs +2 %)
+      static bool attr_ips = false;
+      if (!attr_ips) {
+        cudaError_t e = cudaFuncSetAttribute(k_apply_v4<P, DIR, GS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)C::SMEM);
+        if (e) return e;
+        attr_ips = true;
+      }
+      return launch_pdl(k_apply_v4<P, DIR, GS, true>, (unsigned)grid, (unsigned)C::THREADS, C::SMEM, s, mm, G, u, v,
+                        groups, wait_mode, write_bnd);
+    }
     return launch_pdl(k_apply_v4<P, DIR, GS>, (unsigned)grid, (unsigned)C::THREADS, C::SMEM, s, mm, G, u, v, groups,
                       wait_mode, write_bnd);
   }
