@@ -1396,6 +1396,17 @@ constexpr int kCoarseThreads = 512;
 #define SFMG_COARSE_STENCIL 1
 #endif
 constexpr int kStencilThreads = 768;
+// block-wide sum with a single barrier: the caller alternates partial buffers so that no thread can
+// still be reading a buffer when it is written again (k_coarse_cg_stencil: pq -> red0, ||r||^2 -> red1)
+__device__ __forceinline__ double block_sum_1bar(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+  if (ln == 0) red[w] = v;
+  __syncthreads();
+  double s = ln < (int)((blockDim.x + 31) >> 5) ? red[ln] : 0.0;
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  return s;
+}
 // block-wide sum for the single-CTA CG: warp shuffles, one partial per warp in smem, then every warp
 // reduces the <= 32 partials with shuffles (no serial chain over the partials)
 __device__ __forceinline__ double block_sum_fast(double v, double* red) {
@@ -1414,7 +1425,7 @@ __global__ void __launch_bounds__(kStencilThreads) k_coarse_cg_stencil(MeshDev m
                                                                         double rtol, int maxit) {
   using GL = GLayout<1>;
   __shared__ double sp[kStencilThreads];
-  __shared__ double red[32];
+  __shared__ double red[32], red1[32];
   const int g = threadIdx.x;
   const bool live = g < m.N;
   const int Mx = m.Mx, My = m.My, Mz = m.Mz;
@@ -1494,12 +1505,13 @@ __global__ void __launch_bounds__(kStencilThreads) k_coarse_cg_stencil(MeshDev m
       } else if (!live) {
         q = 0.0;
       }
-      const double pq = block_sum_fast(p * q, red);
+      const double pq = block_sum_1bar(p * q, red);    // 1 barrier (buffers alternate; the rn
+                                                       // barrier and the loop-top one separate reuses)
       if (!(pq > 0.0)) { status = 6; break; }
       const double alpha = rr / pq;
       x += alpha * p;
       r -= alpha * q;
-      const double rn = block_sum_fast(r * r, red);
+      const double rn = block_sum_1bar(r * r, red1);
       p = r + (rn / rr) * p;
       sp[g] = p;   // every read of the old p is before the reductions' barriers
       rr = rn;
