@@ -32,8 +32,11 @@ namespace sfmg {
 //    -39 % at p = 16) and half the constants.
 //  * c_xw: LGL nodes and weights of every order.
 constexpr int kDCopies = 5;
-#ifndef SFMG_EO_COPIES
-#define SFMG_EO_COPIES 6   // 6: one even-odd table per line pass; 2: one for D, one for D^T
+#ifndef SFMG_EO_SHARED_MAXP
+// orders up to this share one even-odd table for D and one for D^T across the line passes (p = 8:
+// Chebyshev step -2.4 %); above it every pass reads its own copy (p = 16 with shared tables: ptxas keeps
+// the 144 coefficients live across passes and spills, 70 -> 105 us)
+#define SFMG_EO_SHARED_MAXP 8
 #endif
 constexpr int dcopies(int P) { return (P % 2 == 1 && P <= 7) ? kDCopies : 1; }
 constexpr int dOffset(int P) {
@@ -106,7 +109,7 @@ __device__ __forceinline__ double dmat(int cp, int idx) {
 template <int P, int SET>
 __device__ __forceinline__ void eo_line(const double (&L)[P + 1], double (&out)[P + 1]) {
   constexpr int N = P + 1, c = P / 2;
-  constexpr int base = eoOffset(P) + (SFMG_EO_COPIES == 2 ? (SET < 3 ? 0 : 3) : SET) * eoSize(P);
+  constexpr int base = eoOffset(P) + (P <= SFMG_EO_SHARED_MAXP ? (SET < 3 ? 0 : 3) : SET) * eoSize(P);
   double ev[c], od[c];
 #pragma unroll
   for (int m = 0; m < c; ++m) {
