@@ -389,7 +389,17 @@ def run_extras(args, sfmg, dev, stream, flush, hbm_peak):
         ta = time_events(lambda: lv.apply(u, v), stream, flush, 20)
         tw = time_events(lambda: lv.apply(u, v), stream, None, 20)
         tc = time_events(lambda: lv.cheb(b, x, 4, 0.1 * lam, 1.1 * lam), stream, flush, 10) / 4
+        # the element kernel alone (library events around each launch, L2 flushed between applies)
+        lv.profile(True)
+        for k in range(10):
+            l2_flush(flush, k)
+            lv.apply(u, v)
+        torch.cuda.synchronize()
+        k_ms, k_n = lv.profile_read(reset=True)
+        lv.profile(False)
+        tk = k_ms * 1e-3 / max(k_n, 1)
         sweep.append({"p": p, "ne": d["nex"], "apply_us": ta * 1e6, "apply_gdofs": lv.N / ta / 1e9,
+                      "apply_kernel_us": tk * 1e6, "apply_kernel_hbm_frac": alg["apply_bytes"] / tk / 1e9 / hbm_peak,
                       "apply_hbm_frac": alg["apply_bytes"] / ta / 1e9 / hbm_peak,
                       "apply_tflops": alg["apply_flops"] / ta / 1e12,
                       "apply_fp64_frac": (alg["apply_flops"] / ta / 1e12 / fp64_tf) if fp64_tf else None,
