@@ -97,6 +97,31 @@ def test_lambda_max_pins(orc):
         assert 0.5 * lam < est <= lam * (1 + 1e-12), (p, est, lam)
 
 
+@pytest.mark.parametrize("p,iters", [(2, 10), (2, 3), (3, 10)])
+def test_lambda_max_closed_form(orc, p, iters):
+    """R9 / P:576-578: after `iters` power steps on D^{-1}A_D the estimate is the D-Rayleigh
+    quotient of the last iterate, lambda = (x^T A x)/(x^T D x) with x proportional to
+    (D^{-1}A_D)^(iters-1) x0 -- formed here from a dense matrix power (no iteration, no normalisation),
+    with x0 = splitmix64(12345) in [-1,1] and the boundary zeroed (R15).  Pins the preconditioned
+    operator (D^{-1}A, not A) and the iteration count (an off-by-one changes the value)."""
+    from paper_1402_5938_b200 import inputs
+    L = orc.Level(3, 3, 3, p, **WARPED)
+    A = L.assemble_dense(0)
+    d = np.diag(A).copy()
+    x0 = inputs.uniform_pm1(12345, L.N)
+    x0[L.mask() == 1] = 0.0
+    x = np.linalg.matrix_power(A / d[:, None], iters - 1) @ x0
+    ref = (x @ A @ x) / (x @ (d * x))
+    est = L.lambda_max(iters, 12345)
+    assert abs(est - ref) <= 1e-13 * ref, (est, ref)
+    if iters == 10:   # the neighbouring counts and the unpreconditioned iteration all differ by far more
+        for k in (iters - 2, iters):
+            y = np.linalg.matrix_power(A / d[:, None], k) @ x0
+            assert abs((y @ A @ y) / (y @ (d * y)) - ref) > 1e-9 * ref
+        y = np.linalg.matrix_power(A, iters - 1) @ x0
+        assert abs((y @ A @ y) / (y @ (d * y)) - ref) > 1e-6 * ref
+
+
 def cheb_error_operator(A, lam_lo, lam_hi, K):
     """T_K((theta I - D^{-1}A)/delta) / T_K(theta/delta): the error propagator of R7."""
     d = np.diag(A)

@@ -148,6 +148,26 @@ def test_element_matrix_brute_force(orc, p):
         np.testing.assert_allclose(K, Kb, rtol=0, atol=1e-12 * np.abs(Kb).max())
 
 
+# coefficient kinds of BASELINE config 4 (mu = 10^(c1 S), contrast 1e4) and of the paper's 3d-var
+# (mu = c0 + c1 sum_i cos^2(2 pi x_i)), each against the brute-force numpy element matrix
+COEFF_KINDS = [
+    (2, 1.0, 2.0, lambda x, y, z: 10.0 ** (2.0 * np.sin(2 * np.pi * x) * np.sin(2 * np.pi * y) * np.sin(2 * np.pi * z))),
+    (3, 1.0, 1e6, lambda x, y, z: 1.0 + 1e6 * (np.cos(2 * np.pi * x) ** 2 + np.cos(2 * np.pi * y) ** 2
+                                                + np.cos(2 * np.pi * z) ** 2)),
+]
+
+
+@pytest.mark.parametrize("kind,c0,c1,mu", COEFF_KINDS, ids=["pow10", "cos2"])
+@pytest.mark.parametrize("p", [1, 2, 3])
+def test_element_matrix_brute_force_coeff_kinds(orc, p, kind, c0, c1, mu):
+    L = orc.Level(2, 2, 2, p, warp=1, amp=0.1, coeff=kind, c0=c0, c1=c1)
+    for e in (0, 3, 6):
+        _, _, X = L.geometry(e)
+        K = L.element_matrix(e)
+        Kb = np_element_matrix(X, p, mu)
+        np.testing.assert_allclose(K, Kb, rtol=0, atol=1e-12 * np.abs(Kb).max())
+
+
 @pytest.mark.parametrize("p", [1, 2, 4])
 def test_element_matrix_affine_kronecker(orc, p):
     nex, ney, nez = 2, 3, 1
