@@ -169,7 +169,8 @@ sfmg_status sfmg_jacobi(sfmg_level lv, const double* d_b, double* d_x, int64_t n
                         double omega, void* stream);
 /* One degree-`degree` Chebyshev-accelerated Jacobi application to A_D x = b on the interval
  * [lam_lo, lam_hi] of D^{-1} A_D (R7, R10): `degree` steps, each one
- * operator apply.  d_x is the initial guess on input and the smoothed iterate on output. */
+ * operator apply.  d_x is the initial guess on input and the smoothed iterate on output.  d_b and
+ * d_x must not alias (the recurrence alternates its iterates through d_x): SFMG_E_ARG if equal. */
 sfmg_status sfmg_cheb(sfmg_level lv, const double* d_b, double* d_x, int64_t n, int32_t degree,
                       double lam_lo, double lam_hi, void* stream);
 /* Load vector of the manufactured solution u* = sin(pi x) sin(pi y) sin(pi z) (rhs_id 1):
@@ -225,7 +226,10 @@ sfmg_status sfmg_hier_level(sfmg_hier h, int32_t l, sfmg_level* out);
 sfmg_status sfmg_hier_lambda(sfmg_hier h, int32_t l, double* h_lambda);
 /* x = V(b) from x = 0: per level nu_pre smoothing applications (Chebyshev or Jacobi), residual,
  * restriction, recursion, prolongation + correction, nu_post applications; coarsest by CG
- * (R11, R13).  No host synchronisation. */
+ * (R11, R13).  No host synchronisation when the coarsest level is a 3-D level of
+ * order <= 2 (the single-CTA device CG; the whole V-cycle is replayed as a CUDA graph).  A 2-D
+ * hierarchy, or a coarsest order > 2 (h-multigrid, NEXT-4), solves the coarsest level with the
+ * host-polled CG, which synchronises the stream every 8 CG iterations. */
 sfmg_status sfmg_vcycle(sfmg_hier h, const double* d_b, double* d_x, void* stream);
 /* mode 0: MG as solver, x <- x + V(b - A x); mode 1: MG-preconditioned CG (Algorithm 1,
  * P:973-991).  x0 = 0 (the input content of d_x is ignored), stop at ||r||_2 <= rtol ||r0||_2

@@ -28,8 +28,9 @@ def _stale(out: str, deps) -> bool:
 
 def _compile(src: str) -> str:
     obj = os.path.join(BUILD, os.path.splitext(src)[0] + ".o")
-    deps = [os.path.join(CSRC, src), os.path.join(CSRC, "sfmg_internal.h"), os.path.join(CSRC, "k_common.cuh"),
-            os.path.join(INCLUDE, "sfmg.h"), __file__]
+    # every header of csrc/ and include/ (conservative: a header edit rebuilds every object)
+    deps = [os.path.join(CSRC, src), __file__] + [os.path.join(d, f) for d in (CSRC, INCLUDE)
+                                                  for f in os.listdir(d) if f.endswith((".h", ".cuh"))]
     if _stale(obj, deps):
         log = obj + ".log"
         cmd = [NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]

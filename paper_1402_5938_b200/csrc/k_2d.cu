@@ -30,11 +30,11 @@ __constant__ double c2_DB[2][q2Offset(kMaxOrder + 1)];   // [quad]: LGL D / Gaus
 __constant__ double c2_B[q2Offset(kMaxOrder + 1)];       // Gauss B (LGL: identity)
 __constant__ double c2_w[2][q2vOffset(kMaxOrder + 1)];   // [quad] quadrature weights
 __constant__ double c2_x[q2vOffset(kMaxOrder + 1)];      // LGL nodes
-static bool g_2d_uploaded[2][kMaxOrder + 1];
+static OncePerDevice g_2d_uploaded[2][kMaxOrder + 1];
 
 cudaError_t upload_2d_tables(int p, int quad) {
   if (p < 1 || p > kMaxOrder || (quad != 0 && quad != 1)) return cudaErrorInvalidValue;
-  if (g_2d_uploaded[quad][p]) return cudaSuccess;
+  return g_2d_uploaded[quad][p].run([&]() -> cudaError_t {
   const int n = p + 1;
   std::vector<double> xn, B, DB, w;
   quad_tables_1d(p, quad, xn, B, DB, w);
@@ -45,8 +45,8 @@ cudaError_t upload_2d_tables(int p, int quad) {
   if (quad == 1 && (e = cudaMemcpyToSymbol(c2_B, B.data(), sizeof(double) * n * n, mo))) return e;
   if ((e = cudaMemcpyToSymbol(c2_w, w.data(), sizeof(double) * n, quad * vq + vo))) return e;
   if ((e = cudaMemcpyToSymbol(c2_x, xn.data(), sizeof(double) * n, vo))) return e;
-  g_2d_uploaded[quad][p] = true;
   return cudaSuccess;
+  });
 }
 
 // tables of order P, quadrature Q into shared memory (B = I for collocated LGL)

@@ -118,11 +118,11 @@ void quad_tables_1d(int p, int quad, std::vector<double>& xn, std::vector<double
     }
 }
 
-static bool g_gauss_uploaded[kMaxOrder + 1];
+static OncePerDevice g_gauss_uploaded[kMaxOrder + 1];
 
 cudaError_t upload_gauss_tables(int p) {
   if (p < 1 || p > kMaxOrder) return cudaErrorInvalidValue;
-  if (g_gauss_uploaded[p]) return cudaSuccess;
+  return g_gauss_uploaded[p].run([&]() -> cudaError_t {
   const int n = p + 1;
   Basis1D L = make_basis(p);
   std::vector<double> gx, gw;
@@ -141,8 +141,8 @@ cudaError_t upload_gauss_tables(int p) {
   if ((e = cudaMemcpyToSymbol(c_qDG, DG.data(), sizeof(double) * n * n, mo))) return e;
   if ((e = cudaMemcpyToSymbol(c_qw, gw.data(), sizeof(double) * n, vo))) return e;
   if ((e = cudaMemcpyToSymbol(c_qxn, L.x.data(), sizeof(double) * n, vo))) return e;
-  g_gauss_uploaded[p] = true;
   return cudaSuccess;
+  });
 }
 
 template <int P> __device__ __forceinline__ double qB(int i, int a) { return c_qB[qOffset(P) + i * (P + 1) + a]; }
@@ -751,11 +751,14 @@ template <int P>
 static cudaError_t geometry_g(const MeshDev& m, double* G, int* bad, cudaStream_t s) {
   constexpr int N = P + 1;
   const size_t smem = sizeof(double) * (3 * N * N * N + 2 * N * N);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_geometry_gauss<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e) return e;
-    attr = true;
+  static OncePerDevice attr;
+  {
+    cudaError_t ea = attr.run([&]() -> cudaError_t {
+      cudaError_t e = cudaFuncSetAttribute(k_geometry_gauss<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e) return e;
+      return cudaSuccess;
+    });
+    if (ea) return ea;
   }
   k_geometry_gauss<P><<<elem_grid(m.E), 256, smem, s>>>(m, G, bad);
   return cudaGetLastError();
@@ -769,13 +772,16 @@ cudaError_t launch_geometry_gauss(const MeshDev& m, double* G, int* bad, cudaStr
 template <int P>
 static cudaError_t apply_g(const MeshDev& m, int bc, const double* G, const double* u, double* v, cudaStream_t s) {
   using C = GaussCfg<P>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_apply_gauss<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
-    if (e) return e;
-    e = cudaFuncSetAttribute(k_apply_gauss<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
-    if (e) return e;
-    attr = true;
+  static OncePerDevice attr;
+  {
+    cudaError_t ea = attr.run([&]() -> cudaError_t {
+      cudaError_t e = cudaFuncSetAttribute(k_apply_gauss<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+      if (e) return e;
+      e = cudaFuncSetAttribute(k_apply_gauss<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+      if (e) return e;
+      return cudaSuccess;
+    });
+    if (ea) return ea;
   }
   const long long groups = (m.E + C::EPB - 1) / C::EPB;
   const unsigned grid = (unsigned)(groups < 148LL * 16 ? groups : 148LL * 16);
@@ -800,11 +806,14 @@ template <int P>
 static cudaError_t load_g(const MeshDev& m, double* f, cudaStream_t s) {
   constexpr int N = P + 1;
   const size_t smem = sizeof(double) * (4 * N * N * N + 2 * N * N);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_load_gauss<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e) return e;
-    attr = true;
+  static OncePerDevice attr;
+  {
+    cudaError_t ea = attr.run([&]() -> cudaError_t {
+      cudaError_t e = cudaFuncSetAttribute(k_load_gauss<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e) return e;
+      return cudaSuccess;
+    });
+    if (ea) return ea;
   }
   k_load_gauss<P><<<elem_grid(m.E), 256, smem, s>>>(m, f);
   return cudaGetLastError();

@@ -32,12 +32,10 @@ namespace sfmg {
 //    -39 % at p = 16) and half the constants.
 //  * c_xw: LGL nodes and weights of every order.
 constexpr int kDCopies = 5;
-#ifndef SFMG_EO_SHARED_MAXP
 // orders up to this share one even-odd table for D and one for D^T across the line passes (p = 8:
 // Chebyshev step -2.4 %); above it every pass reads its own copy (p = 16 with shared tables: ptxas keeps
 // the 144 coefficients live across passes and spills, 70 -> 105 us)
-#define SFMG_EO_SHARED_MAXP 8
-#endif
+constexpr int kEoSharedMaxP = 8;
 constexpr int dcopies(int P) { return (P % 2 == 1 && P <= 7) ? kDCopies : 1; }
 constexpr int dOffset(int P) {
   int s = 0;
@@ -59,11 +57,9 @@ __constant__ double c_Dc[dOffset(kMaxOrder + 1)];
 __constant__ double c_EO[eoOffset(kMaxOrder + 2)];
 __constant__ double c_xw[2][xOffset(kMaxOrder + 1)];
 
-static bool g_uploaded[kMaxOrder + 1];
+static OncePerDevice g_uploaded[kMaxOrder + 1];
 
-cudaError_t upload_order_tables(int p, cudaStream_t s) {
-  (void)s;
-  if (g_uploaded[p]) return cudaSuccess;
+static cudaError_t upload_order_tables_now(int p) {
   Basis1D B = make_basis(p);
   const int n = p + 1;
   cudaError_t e;
@@ -90,10 +86,12 @@ cudaError_t upload_order_tables(int p, cudaStream_t s) {
   }
   e = cudaMemcpyToSymbol(c_xw, B.x.data(), sizeof(double) * n, sizeof(double) * xOffset(p));
   if (e) return e;
-  e = cudaMemcpyToSymbol(c_xw, B.w.data(), sizeof(double) * n, sizeof(double) * (xOffset(kMaxOrder + 1) + xOffset(p)));
-  if (e) return e;
-  g_uploaded[p] = true;
-  return cudaSuccess;
+  return cudaMemcpyToSymbol(c_xw, B.w.data(), sizeof(double) * n, sizeof(double) * (xOffset(kMaxOrder + 1) + xOffset(p)));
+}
+cudaError_t upload_order_tables(int p, cudaStream_t s) {
+  (void)s;
+  if (p < 1 || p > kMaxOrder) return cudaErrorInvalidValue;
+  return g_uploaded[p].run([p] { return upload_order_tables_now(p); });
 }
 
 // ------------------------------------------------------------------------------------------
@@ -109,7 +107,7 @@ __device__ __forceinline__ double dmat(int cp, int idx) {
 template <int P, int SET>
 __device__ __forceinline__ void eo_line(const double (&L)[P + 1], double (&out)[P + 1]) {
   constexpr int N = P + 1, c = P / 2;
-  constexpr int base = eoOffset(P) + (P <= SFMG_EO_SHARED_MAXP ? (SET < 3 ? 0 : 3) : SET) * eoSize(P);
+  constexpr int base = eoOffset(P) + (P <= kEoSharedMaxP ? (SET < 3 ? 0 : 3) : SET) * eoSize(P);
   double ev[c], od[c];
 #pragma unroll
   for (int m = 0; m < c; ++m) {
@@ -223,9 +221,6 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
 // bytes); their bulk copies and L2 prefetches carry an L2 evict-first policy so that the streamed
 // factors do not push u and the RED target v (each touched by up to 8 elements, at different times)
 // out of L2.
-#ifndef SFMG_G_EVICT_FIRST
-#define SFMG_G_EVICT_FIRST 1
-#endif
 __device__ __forceinline__ uint64_t l2_evict_first_policy() {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
@@ -233,18 +228,11 @@ __device__ __forceinline__ uint64_t l2_evict_first_policy() {
 }
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-  if (SFMG_G_EVICT_FIRST) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(l2_evict_first_policy())
-        : "memory");
-  } else {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-  }
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(l2_evict_first_policy())
+      : "memory");
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
@@ -255,17 +243,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
       : "memory");
 }
 
-#ifndef SFMG_G_EF_PREFETCH
-#define SFMG_G_EF_PREFETCH SFMG_G_EVICT_FIRST
-#endif
 __device__ __forceinline__ void bulk_prefetch_l2(const void* src, unsigned bytes) {
-  if (SFMG_G_EF_PREFETCH) {
-    asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(src), "r"(bytes),
-                 "l"(l2_evict_first_policy())
-                 : "memory");
-  } else {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
-  }
+  asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(src), "r"(bytes),
+               "l"(l2_evict_first_policy())
+               : "memory");
 }
 
 __device__ __forceinline__ void fence_proxy_async_smem() {
@@ -301,66 +282,21 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 //             next element TMA-prefetched into L2 (p >= 9: G of one element is up to 236 KB and cannot
 //             be staged).
 //
-// Compile-time knobs.  The defaults are the measured choices; the alternatives are kept so that the
-// A/B builds of tools/build_variant.py can re-measure them (profiles/r01_experiments.md has the numbers).
-#ifndef SFMG_PF_AHEAD
-#define SFMG_PF_AHEAD 1        // !GS: L2 prefetch distance in groups (2 overflows L2 at p = 16)
-#endif
-#ifndef SFMG_RING
-#define SFMG_RING 5            // !GS: register ring depth in k-slices (loads RING - 1 slices ahead)
-#endif
-#ifndef SFMG_V4_SMEM
-#define SFMG_V4_SMEM 52000     // smem budget per block that sets the elements per block (p <= 8)
-#endif
-#ifndef SFMG_V4_THR
-#define SFMG_V4_THR 256        // thread budget per block that sets the elements per block
-#endif
-#ifndef SFMG_RESIDENT_MAX
-#define SFMG_RESIDENT_MAX 0    // > 0: cap the persistent apply's blocks per SM (occupancy sweeps)
-#endif
-#ifndef SFMG_PF_GS
-#define SFMG_PF_GS 2           // GS, long grids: L2 prefetch of group g+2 (3: also g+3)
-#endif
-#ifndef SFMG_PF_START
-#define SFMG_PF_START 0        // 1: L2 prefetch burst at kernel start as well (slower at config 2)
-#endif
-#ifndef SFMG_PF_TOP
-#define SFMG_PF_TOP 0          // !GS: 1 = prefetch the next element at the element top (L2 overflow)
-#endif
-#ifndef SFMG_MINB_HI
-#define SFMG_MINB_HI 1         // p >= 12: blocks per SM requested from ptxas (2 spills)
-#endif
-#ifndef SFMG_EARLY
-#define SFMG_EARLY 1           // register prefetch of the next u column (p <= 11; 2: also p >= 12)
-#endif
-#ifndef SFMG_V5
-#define SFMG_V5 0              // 1: even p >= 4 through k_apply_v5.cuh (two threads per line; slower)
-#endif
-#ifndef SFMG_V5_SMEM_BUDGET
-#define SFMG_V5_SMEM_BUDGET 60000
-#endif
-#ifndef SFMG_APPLY_TRIGGER
-#define SFMG_APPLY_TRIGGER 1   // persistent apply triggers its dependent at its last group; update is PDL
-#endif
-#ifndef SFMG_TRANSPOSED_Y
-#define SFMG_TRANSPOSED_Y 1    // p = 8: y-direction data in a transposed smem array (fewer bank conflicts)
-#endif
-#ifndef SFMG_IPS
-#define SFMG_IPS 1             // plain stores for element-interior nodes when N > 2^24 (see k_apply_v4)
-#endif
-#ifndef SFMG_KSTAGE
-#define SFMG_KSTAGE 0          // !GS, one element per block: first k-slices TMA-staged in free smem
-#endif
+// Tuning constants (measured choices; the rejected alternatives and their times are listed in
+// profiles/r01_experiments.md).
+constexpr int kRing = 5;           // !GS: register ring depth in k-slices (loads kRing - 1 slices ahead)
+constexpr int kV4Smem = 52000;     // smem budget per block that sets the elements per block (p <= 8)
+constexpr int kV4Thr = 256;        // thread budget per block that sets the elements per block
+constexpr int kPfGS = 2;           // GS, long grids: L2 prefetch of group g+2
 // Early programmatic-dependent triggers (v init, Chebyshev update, apply -> update) are used for
 // vectors of at most this many dofs; SFMG_EARLY_MAXN in the environment overrides it (0: never; the
 // tests run both paths).
 constexpr long long kEarlyMaxN = 1ll << 24;
 static bool early_pdl(const MeshDev& m) {
-  static long long thr = -1;
-  if (thr < 0) {
+  static const long long thr = [] {
     const char* e = getenv("SFMG_EARLY_MAXN");
-    thr = e ? atoll(e) : kEarlyMaxN;
-  }
+    return e ? atoll(e) : kEarlyMaxN;
+  }();
   return m.N <= thr;
 }
 
@@ -368,18 +304,13 @@ template <int P, bool GS>
 struct V4Cfg {
   static constexpr int N = P + 1, N2 = N * N, N3 = N2 * N;
   static constexpr int PER_ELEM = (GS ? 8 : 2) * N3 * 8;   // smem bytes per element
-  static constexpr int EPB_SMEM = SFMG_V4_SMEM / PER_ELEM > 0 ? SFMG_V4_SMEM / PER_ELEM : 1;
-  static constexpr int EPB_THR = SFMG_V4_THR / N2 > 0 ? SFMG_V4_THR / N2 : 1;
+  static constexpr int EPB_SMEM = kV4Smem / PER_ELEM > 0 ? kV4Smem / PER_ELEM : 1;
+  static constexpr int EPB_THR = kV4Thr / N2 > 0 ? kV4Thr / N2 : 1;
   static constexpr int EPB = EPB_SMEM < EPB_THR ? EPB_SMEM : EPB_THR;
   static constexpr int THREADS = EPB * N2;
-  // GS == false with one element per block: the first KST factor k-slices of the element (one contiguous
-  // block of the slice-major layout) are TMA-staged into the smem left free by the work arrays
-  static constexpr int KST_FIT = (232448 - EPB * PER_ELEM - 16) / (6 * N2 * 8);
-  static constexpr int KST_WANT = SFMG_KSTAGE < N ? SFMG_KSTAGE : N;
-  static constexpr int KST = (GS || EPB != 1) ? 0 : (KST_WANT < KST_FIT ? KST_WANT : KST_FIT);
-  static constexpr size_t SMEM = (size_t)EPB * PER_ELEM + (size_t)KST * 6 * N2 * 8 + 16;
+  static constexpr size_t SMEM = (size_t)EPB * PER_ELEM + 16;
   static constexpr int MINB_SMEM = (227 * 1024) / (SMEM + 1024) < 8 ? (227 * 1024) / (SMEM + 1024) : 8;
-  static constexpr int MINB = GS ? MINB_SMEM : (P >= 12 ? SFMG_MINB_HI : 2);
+  static constexpr int MINB = GS ? MINB_SMEM : (P >= 12 ? 1 : 2);
 };
 
 // IPS: element-interior nodes (one owner element) take a plain store instead of an fp64 RED (v must be
@@ -396,12 +327,12 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
   // the next group's u column is loaded right after this group's is staged, so it is in flight
   // during the whole element (measured: p = 16 -2.5 %, p <= 8 within noise)
   // (p >= 12: off; the u columns are L2-prefetched instead, which frees 2n registers: p = 16 -2 %)
-  constexpr bool EARLY = (P >= 12) ? (SFMG_EARLY > 1) : (SFMG_EARLY > 0);
+  constexpr bool EARLY = P <= 11;
   // TR: the y-direction data live in a transposed array (index j + n i + n^2 k), so the y-line passes
   // read and write it with the x-lines' conflict-free stride; s0 holds u -> g0 -> w0 -> X (natural layout,
   // x-lines in place), su holds u -> g1 -> w1 -> Y (transposed, y-lines in place), and the z-line pass
   // adds X + Y + Z.  Removes the 2-way bank conflicts of natural-layout y-lines at p = 8.
-  constexpr bool TR = SFMG_TRANSPOSED_Y && GS && P == 8;   // measured: p = 8 step -2 %, p = 4 +1 %
+  constexpr bool TR = GS && P == 8;   // measured: p = 8 step -2 %, p = 4 +1 %
   extern __shared__ __align__(128) double smem[];
   double* sG = smem;                                   // [EPB][k][6][n^2] (GS)
   const int le = threadIdx.x / N2;
@@ -409,9 +340,7 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
   const int t0 = t % N, t1 = t / N;
   double* s0 = smem + (GS ? C::EPB * 6 * N3 : 0) + le * 2 * N3;   // per element: s0, su
   double* su = s0 + N3;
-  constexpr int KST = C::KST;
-  double* sK = smem + C::EPB * (GS ? 8 : 2) * N3;     // [KST][6][n^2] (!GS, EPB == 1)
-  uint64_t* bar = (uint64_t*)(sK + KST * 6 * N2);
+  uint64_t* bar = (uint64_t*)(smem + C::EPB * (GS ? 8 : 2) * N3);
   const double* gE = sG + le * 6 * N3;
   const long long sxy = (long long)m.Mx * m.My;
   const long long gstride = gridDim.x;
@@ -460,21 +389,14 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
   // an L2 prefetch of g+2 deepens the HBM pipeline, which pays in long runs (config 4: 2.68 -> 2.53 ms)
   // but delays the first TMA loads of short ones (config 2: 46.1 -> 48.1 us), so it is used only when
   // each block walks >= 16 groups.  !GS: g+1 (two generations of p >= 9 factors overflow L2).
-  const int PF = GS ? (SFMG_PF_GS >= 2 && ngroups >= 16 * gstride ? SFMG_PF_GS : 1) : SFMG_PF_AHEAD;
+  const int PF = GS ? (ngroups >= 16 * gstride ? kPfGS : 1) : 1;
   if (threadIdx.x == 0) {   // factor prefetches need nothing from the predecessor kernel
     if (GS) {
       mbar_init(bar, 1);
       if (grp < ngroups) bulk_load(sG, G + grp * C::EPB * 6 * N3, group_bytes(grp), bar);
-    } else if (KST > 0) {
-      mbar_init(bar, 1);
-      if (grp < ngroups) bulk_load(sK, G + grp * 6 * N3, KST * 6 * N2 * 8, bar);
-    }
-    if (GS) {
-    } else if (grp < ngroups && PF >= 1) {
+    } else if (grp < ngroups) {
       prefetch_group_l2(grp);
     }
-    if (SFMG_PF_START && PF >= 2 && grp + gstride < ngroups) prefetch_group_l2(grp + gstride);
-    if (SFMG_PF_START && PF >= 3 && grp + 2 * gstride < ngroups) prefetch_group_l2(grp + 2 * gstride);
   }
   // wait_mode 2: u is produced by the predecessor; 1: only v is (wait before the first scatter)
   if (wait_mode == 2) pdl_wait();
@@ -488,7 +410,7 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
     // last group of this block: let a programmatic dependent (the Chebyshev update) launch now; it
     // waits (griddepcontrol.wait) for this grid's completion before reading v.  Small vectors only
     // (config 4 measured 2.51 -> 2.61 ms with it)
-    if (SFMG_APPLY_TRIGGER && m.pdl_early && grp + gstride >= ngroups) pdl_trigger();
+    if (m.pdl_early && grp + gstride >= ngroups) pdl_trigger();
     const long long e = grp * C::EPB + le;
     const bool act = e < m.E;
     int ex = 0, ey = 0, ez = 0;
@@ -499,16 +421,14 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
       const int I = ex * P + t0, J = ey * P + t1;
       bxy = (I == 0) || (I == m.Mx - 1) || (J == 0) || (J == m.My - 1);
     }
-    if (!GS && PF == 1 && SFMG_PF_TOP && threadIdx.x == 0 && grp + gstride < ngroups)
-      prefetch_group_l2(grp + gstride);   // next group's factors, a whole element ahead
     const double* Gg = G + (act ? e : 0) * 6 * N3 + t;   // GS == false: this thread's factor column
-    constexpr int RG = SFMG_RING;                           // ring depth (loads RG - 1 slices ahead)
+    constexpr int RG = kRing;                               // ring depth (loads RG - 1 slices ahead)
     double gb[RG][6];                                       // GS == false: k-slice ring in registers
     if (!GS) {
 #pragma unroll
-      for (int kk = 0; kk < RG - 1 && KST + kk < N; ++kk)
+      for (int kk = 0; kk < RG - 1 && kk < N; ++kk)
 #pragma unroll
-        for (int c = 0; c < 6; ++c) gb[kk][c] = __ldcs(Gg + gofs<N>(c, 0, KST + kk));
+        for (int c = 0; c < 6; ++c) gb[kk][c] = __ldcs(Gg + gofs<N>(c, 0, kk));
     }
     if (TR) {
 #pragma unroll
@@ -569,7 +489,7 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
       }
     }
     __syncthreads();
-    if (GS || KST > 0) {
+    if (GS) {
       mbar_wait(bar, phase);
       phase ^= 1u;
     }
@@ -590,12 +510,11 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
 #pragma unroll
       for (int k = 0; k < N; ++k) {
         double G00, G01, G02, G11, G12, G22;
-        if (GS || k < KST) {
-          const double* Gk = (GS ? gE : sK) + gofs<N>(0, t, k);
+        if (GS) {
+          const double* Gk = gE + gofs<N>(0, t, k);
           G00 = Gk[0]; G01 = Gk[N2]; G02 = Gk[2 * N2]; G11 = Gk[3 * N2]; G12 = Gk[4 * N2]; G22 = Gk[5 * N2];
         } else {
-          constexpr int zk = 0;
-          const int kr = k - KST + zk;   // ring slot index (compile-time after unrolling)
+          const int kr = k;   // ring slot index (compile-time after unrolling)
           if (k + RG - 1 < N) {
 #pragma unroll
             for (int c = 0; c < 6; ++c) gb[(kr + RG - 1) % RG][c] = __ldcs(Gg + gofs<N>(c, 0, k + RG - 1));
@@ -629,13 +548,9 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
         if (GS) {
           fence_proxy_async_smem();
           bulk_load(sG, G + nx * C::EPB * 6 * N3, group_bytes(nx), bar);
-        } else if (KST > 0) {
-          fence_proxy_async_smem();
-          bulk_load(sK, G + nx * 6 * N3, KST * 6 * N2 * 8, bar);
         }
-        if (PF >= 3 && nx + 2 * gstride < ngroups) prefetch_group_l2(nx + 2 * gstride);
-        else if (PF == 2 && nx + gstride < ngroups) prefetch_group_l2(nx + gstride);
-        else if (!GS && PF == 1 && !SFMG_PF_TOP && nx < ngroups) prefetch_group_l2(nx);
+        if (PF == 2 && nx + gstride < ngroups) prefetch_group_l2(nx + gstride);
+        else if (!GS && nx < ngroups) prefetch_group_l2(nx);
       }
     }
     if (!EARLY && grp + gstride < ngroups) {   // next group's u column, in flight during P4-P6
@@ -705,7 +620,6 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
   }
 }
 
-#include "k_apply_v5.cuh"
 
 // ------------------------------------------------------------------------------------------
 // K2 apply, thread per element (p <= 2): the whole element (n^3 <= 27 nodes) lives in registers,
@@ -906,11 +820,27 @@ __global__ void __launch_bounds__(256) k_init(MeshDev m, int bc, const double* _
   if (!early) pdl_trigger();   // after this block's work (see k_cheb_update)
 }
 
+// v = 0 before a p <= 2 standalone apply, whose canonical owner elements store the boundary values
+// (write_bnd).  Pure 16-byte stores, one small block per SM that triggers its programmatic dependent at
+// once, so the apply's blocks start during the zeroing and only their first scatter waits
+// (griddepcontrol.wait).  (For p >= 3 the row-wise k_init + owner-free scatter measured faster; the
+// fused in-kernel init with a grid barrier and this kernel in front of k_apply_v4 were both slower,
+// profiles/r02_experiments.md.)
+constexpr int kZeroThreads = 64;
+__global__ void __launch_bounds__(kZeroThreads) k_zero(double* __restrict__ v, long long n) {
+  pdl_trigger();
+  const long long n2 = n >> 1;   // v is 16-byte aligned (checked by the launcher)
+  const long long q0 = n2 * blockIdx.x / gridDim.x, q1 = n2 * (blockIdx.x + 1) / gridDim.x;
+  double2* v2 = reinterpret_cast<double2*>(v);
+  for (long long q = q0 + threadIdx.x; q < q1; q += blockDim.x) v2[q] = make_double2(0.0, 0.0);
+  if ((n & 1) && blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) v[n - 1] = 0.0;
+}
+
 __global__ void k_cheb_update(MeshDev m, const double* cur, const double* prev, double* out,
                               const double* __restrict__ b, double* y, const double* __restrict__ dinv,
                               double c1, double c2, int early) {
   if (early) pdl_trigger();   // one resident wave: see k_init
-  if (SFMG_APPLY_TRIGGER) pdl_wait();   // launched as the apply's programmatic dependent
+  pdl_wait();   // launched as the apply's programmatic dependent
   for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < m.N; g += (long long)gridDim.x * blockDim.x) {
     const double xc = cur[g];
     const double xp = (c1 != 0.0) ? prev[g] : 0.0;
@@ -1216,72 +1146,43 @@ static cudaError_t launch_pdl(void (*k)(KArgs...), unsigned grid, unsigned block
   return cudaLaunchKernelEx(&cfg, k, args...);
 }
 
+// sets the dynamic smem limit of kernel k once per device and returns its resident blocks per SM
+template <typename K>
+static cudaError_t persistent_blocks(IntPerDevice& cache, K k, int threads, size_t smem, int& per_sm) {
+  return cache.get(per_sm, [&](int& v) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e) return e;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k, threads, smem);
+  });
+}
+
 template <int P, bool DIR>
 static cudaError_t apply_pd(const MeshDev& m, const double* G, const double* u, double* v, int wait_mode,
                             int write_bnd, cudaStream_t s) {
   if constexpr (P <= 2) {
-    static int grid = 0;
-    if (!grid) {
-      int per_sm = 0, dev = 0, sms = 0;
-      cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_apply_tpe<P, DIR>, 128, 0);
-      if (e) return e;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      grid = (per_sm > 0 ? per_sm : 1) * sms;
-    }
+    static IntPerDevice occ;
+    int per_sm = 0;
+    cudaError_t e = persistent_blocks(occ, k_apply_tpe<P, DIR>, 128, 0, per_sm);
+    if (e) return e;
     long long blocks = (m.E + 127) / 128;
-    if (blocks > grid) blocks = grid;
+    if (blocks > (long long)per_sm * num_sms()) blocks = (long long)per_sm * num_sms();
     return launch_pdl(k_apply_tpe<P, DIR>, (unsigned)blocks, 128, 0, s, m, G, u, v, wait_mode, write_bnd);
-  } else if constexpr (SFMG_V5 && P % 2 == 0 && P >= 4) {
-    constexpr bool GS = (P <= 8);
-    using C = V5Cfg<P, GS>;
-    static int resident = 0;
-    static int num_sms = 0;
-    if (!resident) {
-      cudaError_t e = cudaFuncSetAttribute(k_apply_v5<P, DIR, GS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
-      if (e) return e;
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_apply_v5<P, DIR, GS>, C::THREADS, C::SMEM);
-      if (e) return e;
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-      if (resident < 1) resident = 1;
-    }
-    const long long groups = (m.E + C::EPB - 1) / C::EPB;
-    long long grid = (long long)resident * num_sms;
-    if (grid > groups) grid = groups;
-    return launch_pdl(k_apply_v5<P, DIR, GS>, (unsigned)grid, (unsigned)C::THREADS, C::SMEM, s, m, G, u, v, groups,
-                      wait_mode, write_bnd);
   } else {
     constexpr bool GS = (P <= 8);
     using C = V4Cfg<P, GS>;
-    static int resident = 0;   // blocks per SM of the persistent kernel
-    static int num_sms = 0;
-    if (!resident) {
-      cudaError_t e = cudaFuncSetAttribute(k_apply_v4<P, DIR, GS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
-      if (e) return e;
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_apply_v4<P, DIR, GS>, C::THREADS, C::SMEM);
-      if (e) return e;
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-      if (resident < 1) resident = 1;
-      if (SFMG_RESIDENT_MAX > 0 && resident > SFMG_RESIDENT_MAX) resident = SFMG_RESIDENT_MAX;
-    }
+    static IntPerDevice occ, occ_ips;
+    int resident = 0;
+    cudaError_t e = persistent_blocks(occ, k_apply_v4<P, DIR, GS>, C::THREADS, C::SMEM, resident);
+    if (e) return e;
     const long long groups = (m.E + C::EPB - 1) / C::EPB;
-    long long grid = (long long)resident * num_sms;
+    long long grid = (long long)resident * num_sms();
     if (grid > groups) grid = groups;
     MeshDev mm = m;
     mm.pdl_early = early_pdl(m) ? 1 : 0;
-    if (SFMG_IPS && !mm.pdl_early && wait_mode == 1) {   // after the v init (measured: config 4 apply -5 %;
-                                                           // after a Chebyshev update it costs +2 %)
-      static bool attr_ips = false;
-      if (!attr_ips) {
-        cudaError_t e = cudaFuncSetAttribute(k_apply_v4<P, DIR, GS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)C::SMEM);
-        if (e) return e;
-        attr_ips = true;
-      }
+    if (!mm.pdl_early && wait_mode == 1) {   // right after the v init (measured: config 4 apply -5 %; after a
+                                             // Chebyshev update +2 %)
+      int r2 = 0;
+      if ((e = persistent_blocks(occ_ips, k_apply_v4<P, DIR, GS, true>, C::THREADS, C::SMEM, r2))) return e;
       return launch_pdl(k_apply_v4<P, DIR, GS, true>, (unsigned)grid, (unsigned)C::THREADS, C::SMEM, s, mm, G, u, v,
                         groups, wait_mode, write_bnd);
     }
@@ -1338,15 +1239,15 @@ cudaError_t launch_init(const MeshDev& m, int bc, const double* u, double bval, 
   int grid = grid_for((long long)m.My * m.Mz * 32, 256);
   // early trigger only for small vectors: for large ones the init outlasts the apply's first element and
   // the early-started apply blocks slow it down (config 2 46.3 -> 44.0 us; config 4 2.51 -> 3.21 ms)
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
   const int early = early_pdl(m) ? 1 : 0;
-  if (early && grid > 8 * sms) grid = 8 * sms;
+  if (early && grid > 8 * num_sms()) grid = 8 * num_sms();
   k_init<<<grid, 256, 0, s>>>(m, bc, u, bval, v, early);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_zero(double* v, long long n, cudaStream_t s) {
+  if ((uintptr_t)v & 15) return cudaMemsetAsync(v, 0, sizeof(double) * n, s);
+  k_zero<<<num_sms(), kZeroThreads, 0, s>>>(v, n);
   return cudaGetLastError();
 }
 
@@ -1354,20 +1255,13 @@ cudaError_t launch_cheb_update(const MeshDev& m, const double* cur, const double
                                const double* b, double* y, const double* dinv, double c1, double c2,
                                cudaStream_t s) {
   int grid = grid_for(m.N, 256);
-  static int resident = 0;
-  if (!resident) {
-    int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_cheb_update, 256, 0);
-    resident = (per > 0 ? per : 1) * sms;
-  }
+  static IntPerDevice occ;
+  int per = 0;
+  cudaError_t e = occ.get(per, [](int& v) { return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_cheb_update, 256, 0); });
+  if (e) return e;
   const int early = early_pdl(m) ? 1 : 0;
-  if (early && grid > resident) grid = resident;
-  if (SFMG_APPLY_TRIGGER)
-    return launch_pdl(k_cheb_update, (unsigned)grid, 256u, 0, s, m, cur, prev, out, b, y, dinv, c1, c2, early);
-  k_cheb_update<<<grid, 256, 0, s>>>(m, cur, prev, out, b, y, dinv, c1, c2, early);
-  return cudaGetLastError();
+  if (early && grid > per * num_sms()) grid = per * num_sms();
+  return launch_pdl(k_cheb_update, (unsigned)grid, 256u, 0, s, m, cur, prev, out, b, y, dinv, c1, c2, early);
 }
 
 template <int P>
@@ -1395,9 +1289,6 @@ constexpr int kCoarseThreads = 512;
 // boundary nodes dropped (R4).  The CG iteration is then one 27-term register x shared-memory product
 // per row and two block reductions -- the same unpreconditioned CG, x0 = 0, ||r|| <= rtol ||b|| (R13),
 // as k_coarse_cg_smem, which re-ran the element apply (48 factor loads per element) every iteration.
-#ifndef SFMG_COARSE_STENCIL
-#define SFMG_COARSE_STENCIL 1
-#endif
 constexpr int kStencilThreads = 768;
 // block-wide sum with a single barrier: the caller alternates partial buffers so that no thread can
 // still be reading a buffer when it is written again (k_coarse_cg_stencil: pq -> red0, ||r||^2 -> red1)
@@ -1530,28 +1421,25 @@ cudaError_t launch_coarse_cg(const MeshDev& m, const double* G, const double* b,
                              double* p, double* q, double* scal, double rtol, int maxit, cudaStream_t s) {
   if (m.quad) return launch_coarse_cg_gauss(m, G, b, x, r, p, q, scal, rtol, maxit, s);
   if (m.p != 1 && m.p != 2) return cudaErrorInvalidValue;
-  if (SFMG_COARSE_STENCIL && m.p == 1 && m.dim == 3 && m.N <= kStencilThreads) {
+  if (m.p == 1 && m.dim == 3 && m.N <= kStencilThreads) {
     k_coarse_cg_stencil<<<1, kStencilThreads, 0, s>>>(m, G, b, x, scal, rtol, maxit);
     return cudaGetLastError();
   }
   if (m.N <= kCoarseSmemN) {
     const size_t smem = sizeof(double) * 4 * (size_t)m.N;
-    static bool attr1 = false, attr2 = false;
+    static OncePerDevice attr1, attr2;
+    const int lim = (int)(sizeof(double) * 4 * kCoarseSmemN);
     if (m.p == 1) {
-      if (!attr1) {
-        cudaError_t e = cudaFuncSetAttribute(k_coarse_cg_smem<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)(sizeof(double) * 4 * kCoarseSmemN));
-        if (e) return e;
-        attr1 = true;
-      }
+      cudaError_t e = attr1.run([&] {
+        return cudaFuncSetAttribute(k_coarse_cg_smem<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+      });
+      if (e) return e;
       k_coarse_cg_smem<1><<<1, kCoarseThreads, smem, s>>>(m, G, b, x, scal, rtol, maxit);
     } else {
-      if (!attr2) {
-        cudaError_t e = cudaFuncSetAttribute(k_coarse_cg_smem<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)(sizeof(double) * 4 * kCoarseSmemN));
-        if (e) return e;
-        attr2 = true;
-      }
+      cudaError_t e = attr2.run([&] {
+        return cudaFuncSetAttribute(k_coarse_cg_smem<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+      });
+      if (e) return e;
       k_coarse_cg_smem<2><<<1, kCoarseThreads, smem, s>>>(m, G, b, x, scal, rtol, maxit);
     }
     return cudaGetLastError();
@@ -1564,3 +1452,4 @@ cudaError_t launch_coarse_cg(const MeshDev& m, const double* G, const double* b,
 }
 
 }  // namespace sfmg
+

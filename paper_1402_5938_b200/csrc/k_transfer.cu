@@ -14,17 +14,17 @@
 namespace sfmg {
 
 __constant__ double c_I[8][17 * 9];   // c_I[pc-1][i*(pc+1)+a], fine order 2 pc
-static bool g_interp_uploaded[9];
+static OncePerDevice g_interp_uploaded[9];
 
 cudaError_t upload_interp_tables(int pc, cudaStream_t s) {
   (void)s;
   if (pc < 1 || pc > 8) return cudaErrorInvalidValue;
-  if (g_interp_uploaded[pc]) return cudaSuccess;
+  return g_interp_uploaded[pc].run([&]() -> cudaError_t {
   std::vector<double> I = make_interp(pc, 2 * pc);
   cudaError_t e = cudaMemcpyToSymbol(c_I, I.data(), sizeof(double) * I.size(), sizeof(double) * 17 * 9 * (pc - 1));
   if (e) return e;
-  g_interp_uploaded[pc] = true;
   return cudaSuccess;
+  });
 }
 
 // element index -> (ex, ey, ez); E < 2^31 (checked at level creation), so 32-bit unsigned
@@ -183,11 +183,14 @@ template <int PC>
 static cudaError_t prolong_p(const MeshDev& mc, const MeshDev& mf, const double* uc, double* uf, int add,
                              cudaStream_t s) {
   using C = XferCfg<PC>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_prolong<PC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_P);
-    if (e) return e;
-    attr = true;
+  static OncePerDevice attr;
+  {
+    cudaError_t ea = attr.run([&]() -> cudaError_t {
+      cudaError_t e = cudaFuncSetAttribute(k_prolong<PC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_P);
+      if (e) return e;
+      return cudaSuccess;
+    });
+    if (ea) return ea;
   }
   k_prolong<PC><<<(unsigned)mf.E, 256, C::SMEM_P, s>>>(mc, mf, uc, uf, add);
   return cudaGetLastError();
@@ -196,11 +199,14 @@ static cudaError_t prolong_p(const MeshDev& mc, const MeshDev& mf, const double*
 template <int PC>
 static cudaError_t restrict_p(const MeshDev& mc, const MeshDev& mf, const double* rf, double* rc, cudaStream_t s) {
   using C = XferCfg<PC>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_restrict<PC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_R);
-    if (e) return e;
-    attr = true;
+  static OncePerDevice attr;
+  {
+    cudaError_t ea = attr.run([&]() -> cudaError_t {
+      cudaError_t e = cudaFuncSetAttribute(k_restrict<PC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_R);
+      if (e) return e;
+      return cudaSuccess;
+    });
+    if (ea) return ea;
   }
   cudaError_t e = cudaMemsetAsync(rc, 0, sizeof(double) * mc.N, s);
   if (e) return e;
@@ -338,19 +344,19 @@ constexpr int hOffset(int P) {
   return s;
 }
 __constant__ double c_H[hOffset(17)];   // per order: H_0 then H_1, [i][a]
-static bool g_h_uploaded[17];
+static OncePerDevice g_h_uploaded[17];
 
 cudaError_t upload_h_tables(int p) {
   if (p < 1 || p > 16) return cudaErrorInvalidValue;
-  if (g_h_uploaded[p]) return cudaSuccess;
+  return g_h_uploaded[p].run([&]() -> cudaError_t {
   const int n = p + 1;
   for (int sc = 0; sc < 2; ++sc) {
     std::vector<double> H = make_h_interp(p, sc);
     cudaError_t e = cudaMemcpyToSymbol(c_H, H.data(), sizeof(double) * n * n, sizeof(double) * (hOffset(p) + sc * n * n));
     if (e) return e;
   }
-  g_h_uploaded[p] = true;
   return cudaSuccess;
+  });
 }
 
 template <int P>
@@ -467,11 +473,14 @@ template <int P>
 static cudaError_t prolong_hp_p(const MeshDev& mc, const MeshDev& mf, const double* uc, double* uf, int add,
                                 cudaStream_t s) {
   constexpr size_t smem = sizeof(double) * 3 * (P + 1) * (P + 1) * (P + 1);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_prolong_hp<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e) return e;
-    attr = true;
+  static OncePerDevice attr;
+  {
+    cudaError_t ea = attr.run([&]() -> cudaError_t {
+      cudaError_t e = cudaFuncSetAttribute(k_prolong_hp<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e) return e;
+      return cudaSuccess;
+    });
+    if (ea) return ea;
   }
   k_prolong_hp<P><<<(unsigned)mf.E, 256, smem, s>>>(mc, mf, uc, uf, add);
   return cudaGetLastError();
@@ -480,11 +489,14 @@ static cudaError_t prolong_hp_p(const MeshDev& mc, const MeshDev& mf, const doub
 template <int P>
 static cudaError_t restrict_hp_p(const MeshDev& mc, const MeshDev& mf, const double* rf, double* rc, cudaStream_t s) {
   constexpr size_t smem = sizeof(double) * 3 * (P + 1) * (P + 1) * (P + 1);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_restrict_hp<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e) return e;
-    attr = true;
+  static OncePerDevice attr;
+  {
+    cudaError_t ea = attr.run([&]() -> cudaError_t {
+      cudaError_t e = cudaFuncSetAttribute(k_restrict_hp<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e) return e;
+      return cudaSuccess;
+    });
+    if (ea) return ea;
   }
   cudaError_t e = cudaMemsetAsync(rc, 0, sizeof(double) * mc.N, s);
   if (e) return e;

@@ -164,9 +164,9 @@ static cudaError_t element_kernel(sfmg_level_s* lv, int bc, const double* u, dou
 
 static cudaError_t op_apply(sfmg_level_s* lv, int bc, const double* u, double* v, cudaStream_t s) {
   cudaError_t e;
-  if (lv->p <= 2 && !lv->m.quad && lv->m.dim == 3) {
-    e = cudaMemsetAsync(v, 0, sizeof(double) * lv->N, s);
-    if (e) return e;
+  if (lv->p <= 2 && !lv->m.quad && lv->m.dim == 3) {   // zero v, then the thread-per-element kernel, whose
+                                                       // canonical owner elements store (I - M) u
+    if ((e = launch_zero(v, lv->N, s))) return e;
     return element_kernel(lv, bc, u, v, 1, 1, s);
   }
   e = launch_init(lv->m, bc, u, 0.0, v, s);
@@ -433,8 +433,8 @@ sfmg_status sfmg_lambda_max(sfmg_level lv, int32_t iters, uint64_t seed, double*
 
 sfmg_status sfmg_cheb(sfmg_level lv, const double* d_b, double* d_x, int64_t n, int32_t degree, double lam_lo,
                       double lam_hi, void* stream) {
-  if (!lv || !d_b || !d_x || degree < 1 || !(lam_hi > lam_lo) || !(lam_lo > 0.0)) {
-    set_error("bad argument to sfmg_cheb");
+  if (!lv || !d_b || !d_x || d_b == d_x || degree < 1 || !(lam_hi > lam_lo) || !(lam_lo > 0.0)) {
+    set_error("bad argument to sfmg_cheb (b and x must be distinct vectors)");
     return SFMG_E_ARG;
   }
   if (n != lv->N) { set_error("vector length != N"); return SFMG_E_ARG; }
@@ -913,7 +913,9 @@ static cudaError_t vcycle_level(sfmg_hier_s* h, size_t l, const double* b, doubl
 // later call launches the instantiated graph on the caller's stream.  SFMG_NO_GRAPH=1 disables it.
 static cudaError_t vcycle(sfmg_hier_s* h, const double* b, double* x, cudaStream_t s) {
   static const bool no_graph = getenv("SFMG_NO_GRAPH") && getenv("SFMG_NO_GRAPH")[0] == '1';
-  if (no_graph || h->host_coarse) return vcycle_level(h, 0, b, x, s);   // host-polled coarse CG: eager
+  bool prof = false;   // per-launch event timing (sfmg_profile_*) cannot be recorded inside a capture
+  for (const sfmg_level_s* L : h->lv) prof = prof || L->prof;
+  if (no_graph || h->host_coarse || prof) return vcycle_level(h, 0, b, x, s);   // eager
   if (h->vc_exec && h->vc_b == b && h->vc_x == x) {
     h->fine_applies += h->vc_fine_applies;
     return cudaGraphLaunch(h->vc_exec, s);

@@ -1,7 +1,9 @@
 // Internal declarations of libsfmg (not part of the ABI).
 #pragma once
 #include <cuda_runtime.h>
+#include <atomic>
 #include <cstdint>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -14,6 +16,59 @@ constexpr int kRedBlocks = 592;   // 4 x 148 SMs: fixed grid of the deterministi
 constexpr int kRedSlots = 4;      // partial sums per reduction pass
 // scalar slots of the general (flag-gated) coarse CG
 constexpr int kCgcBB = 20, kCgcRho = 21, kCgcPQ = 22, kCgcRn = 23, kCgcBeta = 24, kCgcFlag = 25, kCgcIt = 26;
+
+// Per-device lazy state.  __constant__ tables, kernel attributes and occupancy figures exist once per
+// device (CUDA context), so every "done" flag and cached number is keyed by the ordinal of the calling
+// thread's current device, and first-time work runs under a mutex (thread-safe; a level built on a
+// second GPU of the same process uploads its own tables).
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= kMaxDevices) d = 0;
+  return d;
+}
+// f() -> cudaError_t runs until it first succeeds on each device
+struct OncePerDevice {
+  std::mutex mu;
+  std::atomic<bool> done[kMaxDevices] = {};
+  template <class F>
+  cudaError_t run(F f) {
+    const int d = current_device();
+    if (done[d].load(std::memory_order_acquire)) return cudaSuccess;
+    std::lock_guard<std::mutex> g(mu);
+    if (done[d].load(std::memory_order_relaxed)) return cudaSuccess;
+    cudaError_t e = f();
+    if (e == cudaSuccess) done[d].store(true, std::memory_order_release);
+    return e;
+  }
+};
+// an int computed once per device by f(int& out) -> cudaError_t (occupancy, SM counts)
+struct IntPerDevice {
+  std::mutex mu;
+  std::atomic<int> val[kMaxDevices] = {};
+  template <class F>
+  cudaError_t get(int& out, F f) {
+    const int d = current_device();
+    out = val[d].load(std::memory_order_acquire);
+    if (out) return cudaSuccess;
+    std::lock_guard<std::mutex> g(mu);
+    out = val[d].load(std::memory_order_relaxed);
+    if (out) return cudaSuccess;
+    int v = 0;
+    cudaError_t e = f(v);
+    if (e) return e;
+    if (v < 1) v = 1;
+    val[d].store(v, std::memory_order_release);
+    out = v;
+    return cudaSuccess;
+  }
+};
+inline int num_sms() {
+  static IntPerDevice cache;
+  int n = 0;
+  cache.get(n, [](int& v) { return cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, current_device()); });
+  return n;
+}
 
 // Mesh + problem description passed by value to kernels.
 struct MeshDev {
@@ -114,6 +169,8 @@ cudaError_t upload_order_tables(int p, cudaStream_t s);
 cudaError_t launch_geometry(const MeshDev& m, double* G, int* bad, cudaStream_t s);
 // v = bnd ? (u ? u[g] : bval) : 0  (bc 0);  v = 0  (bc 1)
 cudaError_t launch_init(const MeshDev& m, int bc, const double* u, double bval, double* v, cudaStream_t s);
+// v = 0 (one small block per SM, programmatic trigger at block start: the next apply overlaps it)
+cudaError_t launch_zero(double* v, long long n, cudaStream_t s);
 // v += A(M u) on interior rows (bc 0) or all rows (bc 1); v must be initialised.  Launched with
 // programmatic dependent launch: wait_mode 1 = only v comes from the preceding kernel (wait before
 // the first scatter), 2 = u does too (wait before the gather).  write_bnd (bc 0): the canonical

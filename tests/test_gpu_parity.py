@@ -280,3 +280,39 @@ def test_apply_host_pipelined_slabs(S, orc, d, bc):
         assert rel_err(got, ref, scale) <= 1e-11, slabs
         np.testing.assert_allclose(got, dev, rtol=0, atol=1e-14 * scale)
     g.host_pipeline(0)
+
+
+def test_cheb_rejects_aliased_b_x(S):
+    """sfmg_cheb alternates its iterates through x, so b == x would be overwritten mid-recurrence:
+    the ABI rejects it (SFMG_E_ARG) and leaves x untouched."""
+    import torch
+    lv = gpu_level(S, inputs.problem(2, 4, **WARP))
+    x = to_gpu(inputs.uniform_pm1(3, lv.N))
+    x0 = x.clone()
+    with pytest.raises(S.SfmgError):
+        lv.cheb(x, x, 4, 0.1, 1.1)
+    torch.cuda.synchronize()
+    assert torch.equal(x, x0)
+
+
+def test_repeated_standalone_applies(S, orc):
+    """The standalone apply initialises v inside its persistent grid and synchronises the grid on a
+    per-level barrier word pair that returns to its initial state after every launch: back-to-back
+    applies (stream-ordered, programmatic-dependent launches) into the same and into different outputs
+    all match the oracle, for the thread-per-element (p <= 2) and persistent (p >= 3) kernels."""
+    import torch
+    for p in (1, 2, 4, 8, 16):
+        d = inputs.problem(2, p, ney=3, nez=2, **WARP)
+        lv = gpu_level(S, d)
+        o = orc_level(orc, d, tier=3)
+        us = [inputs.uniform_pm1(40 + k, lv.N) for k in range(3)]
+        refs = [o.apply(u, 0, 3) for u in us]
+        ug = [to_gpu(u) for u in us]
+        vs = [torch.full_like(ug[0], 7.0) for _ in range(3)]
+        for rep in range(4):
+            for k in range(3):
+                lv.apply(ug[k], vs[k])
+        torch.cuda.synchronize()
+        for k in range(3):
+            err = rel_err(vs[k].cpu().numpy(), refs[k], np.abs(refs[k]).max())
+            assert err <= 1e-11, (p, k, err)
