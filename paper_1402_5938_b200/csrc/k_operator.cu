@@ -58,6 +58,8 @@ __constant__ double c_EO[eoOffset(kMaxOrder + 2)];
 __constant__ double c_xw[2][xOffset(kMaxOrder + 1)];
 
 static OncePerDevice g_uploaded[kMaxOrder + 1];
+// shared-memory tables of the k-split apply (k_apply_ks.cuh), laid out on the host
+static cudaError_t upload_ks_tables(int p, const std::vector<double>& D, const std::vector<double>& eo6);
 
 static cudaError_t upload_order_tables_now(int p) {
   Basis1D B = make_basis(p);
@@ -83,6 +85,7 @@ static cudaError_t upload_order_tables_now(int p) {
     }
     e = cudaMemcpyToSymbol(c_EO, tab.data(), sizeof(double) * tab.size(), sizeof(double) * eoOffset(p));
     if (e) return e;
+    if ((e = upload_ks_tables(p, B.D, tab))) return e;
   }
   e = cudaMemcpyToSymbol(c_xw, B.x.data(), sizeof(double) * n, sizeof(double) * xOffset(p));
   if (e) return e;
@@ -104,8 +107,11 @@ __device__ __forceinline__ double dmat(int cp, int idx) {
 }
 
 // out = M L for one 1-D line, M = D (SET 0..2) or D^T (SET 3..5), in the even-odd form above.
+// zo: an offset that is always 0 but opaque to the compiler (k_apply_ks passes one derived from its
+// element index), so the table loads stay inside the element loop as uniform loads feeding DFMA
+// instead of being hoisted into (and spilled from) the per-thread register file
 template <int P, int SET>
-__device__ __forceinline__ void eo_line(const double (&L)[P + 1], double (&out)[P + 1]) {
+__device__ __forceinline__ void eo_line(const double (&L)[P + 1], double (&out)[P + 1], int zo = 0) {
   constexpr int N = P + 1, c = P / 2;
   constexpr int base = eoOffset(P) + (P <= kEoSharedMaxP ? (SET < 3 ? 0 : 3) : SET) * eoSize(P);
   double ev[c], od[c];
@@ -116,18 +122,18 @@ __device__ __forceinline__ void eo_line(const double (&L)[P + 1], double (&out)[
   }
 #pragma unroll
   for (int i = 0; i < c; ++i) {
-    double S = 0.0, T = c_EO[base + 2 * c * c + i] * L[c];
+    double S = 0.0, T = c_EO[base + 2 * c * c + i + zo] * L[c];
 #pragma unroll
     for (int m = 0; m < c; ++m) {
-      S = fma(c_EO[base + i * c + m], od[m], S);
-      T = fma(c_EO[base + c * c + i * c + m], ev[m], T);
+      S = fma(c_EO[base + i * c + m + zo], od[m], S);
+      T = fma(c_EO[base + c * c + i * c + m + zo], ev[m], T);
     }
     out[i] = S + T;
     out[N - 1 - i] = S - T;
   }
   double M = 0.0;
 #pragma unroll
-  for (int m = 0; m < c; ++m) M = fma(c_EO[base + 2 * c * c + c + m], od[m], M);
+  for (int m = 0; m < c; ++m) M = fma(c_EO[base + 2 * c * c + c + m + zo], od[m], M);
   out[c] = M;
 }
 
@@ -620,6 +626,52 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
   }
 }
 
+
+#include "k_apply_ks.cuh"
+
+template <int P>
+static void build_ks_tables(const std::vector<double>& D, const std::vector<double>& eo6, double* out) {
+  using C = KsCfg<P>;
+  using HT = HalfTab<P>;
+  constexpr int N = P + 1, c = HT::c, R = HT::R, EOS = C::EOS;
+  const double* set0 = eo6.data();             // even-odd D
+  const double* set3 = eo6.data() + 3 * EOS;   // even-odd D^T
+  for (int q = 0; q < EOS; ++q) out[q] = set0[q];
+  for (int mat = 0; mat < 2; ++mat)
+    for (int hh = 0; hh < 2; ++hh) {
+      const double* tab = mat ? set3 : set0;
+      double* h = out + EOS + mat * C::HMS + hh * HT::HSTR;
+      for (int r = 0; r < HT::HSTR; ++r) {
+        double val = 0.0;   // rows past c (hh = 1, c odd) and the padding stay zero
+        if (r < R * c) {
+          const int i = hh * R + r / c;
+          if (i < c) val = tab[i * c + r % c];
+        } else if (r < 2 * R * c) {
+          const int i = hh * R + (r - R * c) / c;
+          if (i < c) val = tab[c * c + i * c + (r - R * c) % c];
+        } else if (r < 2 * R * c + R) {
+          const int i = hh * R + (r - 2 * R * c);
+          if (i < c) val = tab[2 * c * c + i];
+        } else if (r < 2 * R * c + R + c) {
+          val = tab[2 * c * c + c + (r - 2 * R * c - R)];
+        }
+        h[r] = val;
+      }
+    }
+  for (int q = 0; q < N * N; ++q) out[EOS + 2 * C::HMS + q] = D[q];
+}
+
+static cudaError_t upload_ks_tables(int p, const std::vector<double>& D, const std::vector<double>& eo6) {
+  if (p < kKsMinP || p % 2) return cudaSuccess;
+  std::vector<double> t(kKsTabMax, 0.0);
+  switch (p) {
+    case 12: build_ks_tables<12>(D, eo6, t.data()); break;
+    case 14: build_ks_tables<14>(D, eo6, t.data()); break;
+    case 16: build_ks_tables<16>(D, eo6, t.data()); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaMemcpyToSymbol(g_kstab, t.data(), sizeof(double) * kKsTabMax, sizeof(double) * kKsTabMax * ((p - 12) / 2));
+}
 
 // ------------------------------------------------------------------------------------------
 // K2 apply, thread per element (p <= 2): the whole element (n^3 <= 27 nodes) lives in registers,
@@ -1156,6 +1208,51 @@ static cudaError_t persistent_blocks(IntPerDevice& cache, K k, int threads, size
   });
 }
 
+// The k-split cluster kernel is correct (parity-tested) but measured slower than k_apply_v4 at p = 16
+// (config 3: 76 vs 59.5 us per element-kernel launch; profiles/r02_experiments.md), so it is opt-in:
+// SFMG_KSPLIT=1.
+static bool ks_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("SFMG_KSPLIT");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
+template <int P, bool DIR, bool IPS>
+static cudaError_t launch_ks(const MeshDev& m, const double* G, const double* u, double* v, int wait_mode,
+                             int write_bnd, cudaStream_t s) {
+  using C = KsCfg<P>;
+  static IntPerDevice clusters;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.blockDim = dim3(C::THREADS);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  int ncl = 0;
+  cudaError_t e = clusters.get(ncl, [&](int& n) {
+    cudaError_t r = cudaFuncSetAttribute(k_apply_ks<P, DIR, IPS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)C::SMEM);
+    if (r) return r;
+    cudaLaunchConfig_t q = cfg;
+    q.gridDim = dim3(2 * num_sms());
+    q.numAttrs = 1;
+    return cudaOccupancyMaxActiveClusters(&n, k_apply_ks<P, DIR, IPS>, &q);
+  });
+  if (e) return e;
+  long long grid = ncl < m.E ? ncl : m.E;
+  cfg.gridDim = dim3((unsigned)(2 * grid));
+  return cudaLaunchKernelEx(&cfg, k_apply_ks<P, DIR, IPS>, m, G, u, v, wait_mode, write_bnd);
+}
+
 template <int P, bool DIR>
 static cudaError_t apply_pd(const MeshDev& m, const double* G, const double* u, double* v, int wait_mode,
                             int write_bnd, cudaStream_t s) {
@@ -1168,6 +1265,15 @@ static cudaError_t apply_pd(const MeshDev& m, const double* G, const double* u, 
     if (blocks > (long long)per_sm * num_sms()) blocks = (long long)per_sm * num_sms();
     return launch_pdl(k_apply_tpe<P, DIR>, (unsigned)blocks, 128, 0, s, m, G, u, v, wait_mode, write_bnd);
   } else {
+    if constexpr (P >= kKsMinP && P % 2 == 0) {   // even orders: the even-odd line products keep the
+                                                   // kernel within the register file (odd p spills)
+      if (ks_enabled()) {
+        MeshDev mm = m;
+        mm.pdl_early = early_pdl(m) ? 1 : 0;
+        if (!mm.pdl_early && wait_mode == 1) return launch_ks<P, DIR, true>(mm, G, u, v, wait_mode, write_bnd, s);
+        return launch_ks<P, DIR, false>(mm, G, u, v, wait_mode, write_bnd, s);
+      }
+    }
     constexpr bool GS = (P <= 8);
     using C = V4Cfg<P, GS>;
     static IntPerDevice occ, occ_ips;
@@ -1453,3 +1559,9 @@ cudaError_t launch_coarse_cg(const MeshDev& m, const double* G, const double* b,
 
 }  // namespace sfmg
 
+
+#ifdef SFMG_KS_DBG
+extern "C" int sfmg_ksdbg_read(unsigned long long* out, int n) {
+  return (int)cudaMemcpyFromSymbol(out, sfmg::g_ksdbg, sizeof(unsigned long long) * n);
+}
+#endif

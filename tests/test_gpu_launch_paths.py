@@ -26,7 +26,7 @@ import oracle
 from paper_1402_5938_b200 import inputs, sfmg
 oracle.build()
 out = {}
-for p in (3, 4, 5, 8, 9, 12, 16):
+for p in (3, 4, 5, 8, 9, 12, 14, 16):
     d = inputs.problem(2, p, ney=2, nez=2, warp=1, amp=0.1, coeff=1, c0=1.0, c1=3.0)
     g = sfmg.Level(sfmg.Problem.from_dict(d))
     o = oracle.Level(d["nex"], d["ney"], d["nez"], p, 1, 0.1, 1, 1.0, 3.0, eager=True, tier=3, geom_tier=2)
@@ -45,9 +45,11 @@ print(json.dumps(out))
 """
 
 
-@pytest.mark.parametrize("maxn", ["0", str(1 << 24)], ids=["completion_ordered", "early_triggers"])
-def test_launch_schedules_match_oracle(maxn):
-    env = dict(os.environ, SFMG_EARLY_MAXN=maxn)
+@pytest.mark.parametrize("maxn,ksplit", [("0", "0"), (str(1 << 24), "0"), ("0", "1"), (str(1 << 24), "1")],
+                         ids=["completion_ordered", "early_triggers", "ksplit_completion_ordered", "ksplit_early"])
+def test_launch_schedules_match_oracle(maxn, ksplit):
+    """ksplit = 1 routes even p >= 12 to the k-split cluster kernel (k_apply_ks.cuh, opt-in)."""
+    env = dict(os.environ, SFMG_EARLY_MAXN=maxn, SFMG_KSPLIT=ksplit)
     r = subprocess.run([sys.executable, "-c", SCRIPT % {"root": ROOT}], env=env, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
