@@ -136,9 +136,20 @@ def replica_value(n_dofs: int, world: int, t_max: float) -> float:
 
 
 # ------------------------------------------------------------------------------------------ oracle (CPU)
-def oracle_vcycle_sample(iterations):
-    """Config-5 p-MG on the oracle (O3 sum-factorised tier, as it stands): hierarchy setup and one
-    V-cycle timed; the PCG solve time is extrapolated as iterations x (V-cycle + one fine apply)."""
+def cpu_model():
+    """Host CPU model name (lscpu) reported beside every oracle time."""
+    try:
+        for line in subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout.splitlines():
+            if line.startswith("Model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def oracle_config5_solve():
+    """Config-5 p-MG PCG solve on the oracle (O3 sum-factorised tier, as it stands), measured end to end:
+    hierarchy setup (geometry, diagonals, 10 power iterations per level) and the whole solve."""
     import oracle
     oracle.build()
     d = inputs.CONFIG5
@@ -147,17 +158,30 @@ def oracle_vcycle_sample(iterations):
                     d.get("c0", 1.0), d.get("c1", 0.0))
     t1 = time.perf_counter()
     b = H.levels[0].load_vector(1)
-    H.vcycle(b)              # the first V-cycle still pays one-time costs (caches, first-touch)
+    r = H.solve(b, mode=1, rtol=1e-8, maxit=200)
     t2 = time.perf_counter()
-    H.vcycle(b)
-    t3 = time.perf_counter()
-    H.levels[0].apply(b, 0, 3)
-    t4 = time.perf_counter()
-    vc, ap = t3 - t2, t4 - t3
-    return {"vcycle_ms": vc * 1e3, "setup_s": t1 - t0, "solve_ms_est": iterations * (vc + ap) * 1e3,
-            "cores": oracle.get_threads(), "kind": "oracle",
-            "sample": "config-5 hierarchy setup + 2 V-cycles (the second timed) + 1 fine apply (O3 tier); "
-                      "solve time = %d x (V-cycle + apply)" % iterations}
+    return {"solve_ms": (t2 - t1) * 1e3, "setup_s": t1 - t0, "pcg_iterations": r["iterations"],
+            "converged": r["converged"], "cores": oracle.get_threads(), "cpu": cpu_model(), "kind": "oracle",
+            "sample": "whole config-5 MG-PCG solve to 1e-8 (O3 tier), measured"}
+
+
+def oracle_cheb_sample(d, seed, ne=4):
+    """The oracle's degree-4 Chebyshev application (O2 direct-quadrature applies, as it stands) on a
+    bounded sample: the workload's order, warp and coefficient on ne^3 elements; GDoF/s per step =
+    sample dofs / (time / 4)."""
+    import oracle
+    oracle.build()
+    L = oracle.Level(ne, ne, ne, d["p"], d.get("warp", 0), d.get("amp", 0.0), d.get("coeff", 0), d.get("c0", 1.0),
+                     d.get("c1", 0.0), eager=True, geom_tier=2, tier=2)
+    u = inputs.uniform_pm1(seed, L.N)
+    lam = L.lambda_max(10, inputs.POWER_SEED)
+    L.cheb(np.zeros(L.N), u, 4, 0.1 * lam, 1.1 * lam)
+    t0 = time.perf_counter()
+    L.cheb(np.zeros(L.N), u, 4, 0.1 * lam, 1.1 * lam)
+    dt = time.perf_counter() - t0
+    return {"value": L.N / (dt / 4) / 1e9, "unit": UNIT, "cores": oracle.get_threads(), "cpu": cpu_model(),
+            "kind": "oracle", "sample": "degree-4 Chebyshev (O2 applies) on %d^3 elements at p=%d, N=%d" % (
+                ne, d["p"], L.N)}
 
 
 def oracle_apply_sample(d, seed, target_s=10.0):
@@ -294,24 +318,27 @@ def run_gpu(args, rank, world, local_rank):
     # the events stop the kernel from overlapping its predecessor)
     lv.profile(True)
     kreps = max(3, min(args.steps, 50))
-    for k in range(kreps):
+    for k in range(kreps):   # one element-kernel launch per L2 flush: every timed launch is cold
         l2_flush(flush, k)
-        step([torch.cuda.Event(enable_timing=True) for _ in range(4)])
+        lv.apply(u, v)
     torch.cuda.synchronize()
     k_ms, k_launches = lv.profile_read(reset=True)
     lv.profile(False)
     t_kernel = max_over_ranks(k_ms * 1e-3 / k_launches)
-    traffic = None
-    try:   # dram read + write bytes per launch of this kernel from the committed ncu --set full capture
-        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as fh:
-            tj = json.load(fh)
-        traffic = tj["dram_bytes_read"] + tj["dram_bytes_write"]
-    except Exception:
-        pass
+    traffic, traffic_src = None, None
+    for tf in ("r02_traffic.json", "r01_traffic.json"):   # dram read + write bytes per launch of this kernel
+        try:                                                 # from the committed ncu --set full capture
+            with open(os.path.join(ROOT, "profiles", tf)) as fh:
+                tj = json.load(fh)
+            traffic = tj["dram_bytes_read"] + tj["dram_bytes_write"]
+            traffic_src = "profiles/%s (ncu --set full, dram__bytes_read.sum + write.sum)" % tf
+            break
+        except Exception:
+            pass
     roof = {"bound": "hbm", "achieved": alg["apply_bytes"] / t_kernel / 1e9, "peak": hbm_peak, "unit": "GB/s",
             "frac": alg["apply_bytes"] / t_kernel / 1e9 / hbm_peak, "traffic": traffic,
-            "traffic_source": "profiles/r01_traffic.json (ncu --set full, dram__bytes_read.sum + write.sum)",
-            "kernel": "k_apply_v4<8,DIR,GS> element kernel (apply + Chebyshev launches; %d launches, %.2f us mean)"
+            "traffic_source": traffic_src,
+            "kernel": "k_apply_v4<8,DIR,GS> element kernel (%d launches, each right after an L2 flush, %.2f us mean)"
                       % (k_launches, t_kernel * 1e6),
             "peak_kind": peak_kind, "algorithmic_bytes_per_launch": alg["apply_bytes"],
             "abi_apply_us": t_apply * 1e6, "abi_apply_frac": alg["apply_bytes"] / t_apply / 1e9 / hbm_peak}
@@ -355,21 +382,37 @@ def run_gpu(args, rank, world, local_rank):
            "roofline": roof, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
            "clocks": clk.summary()}
     out.update(extras)
+    cpu_extra = {}
     if rank == 0 and world == 1 and not args.no_cpu:
         gd, cores, sample = oracle_apply_sample(d, inputs.SEEDS[2])
-        out["cpu_baseline"] = {"value": gd, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample}
-        if not args.quick:   # the oracle also at T=1
+        out["cpu_baseline"] = {"value": gd, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
+                               "cpu": cpu_model()}
+        if not args.quick:   # the oracle also at T=1, its Chebyshev step, configs 3-5
             import oracle
             oracle.set_threads(1)
             g1, c1, s1 = oracle_apply_sample(d, inputs.SEEDS[2], target_s=4.0)
             oracle.set_threads(cores)
-            out["cpu_baseline_t1"] = {"value": g1, "unit": UNIT, "cores": c1, "kind": "oracle", "sample": s1}
-            # the oracle's O3 time to solution for config 5, bounded: setup + one V-cycle,
-            # solve time = V-cycle time x the GPU's PCG iteration count (plus one fine apply each)
-            if "config5_pmg_pcg" in out:
-                out["cpu_baseline_config5"] = oracle_vcycle_sample(out["config5_pmg_pcg"]["pcg_iterations"])
+            cpu_extra["cpu_baseline_t1"] = {"value": g1, "unit": UNIT, "cores": c1, "kind": "oracle", "sample": s1}
+            cpu_extra["cpu_baseline_cheb_step"] = oracle_cheb_sample(d, inputs.SEEDS[2])
+            cpu_extra["cpu_baseline_config3"] = {}
+            for p in (1, 2, 4, 8, 16):
+                gp, cp_, sp = oracle_apply_sample(inputs.CONFIG3[p], inputs.SEEDS[3], target_s=3.0)
+                cpu_extra["cpu_baseline_config3"]["p%d" % p] = {"value": gp, "unit": UNIT, "cores": cp_, "sample": sp}
+            g4, c4, s4 = oracle_apply_sample(inputs.CONFIG4, inputs.SEEDS[4], target_s=3.0)
+            cpu_extra["cpu_baseline_config4"] = {"value": g4, "unit": UNIT, "cores": c4, "kind": "oracle", "sample": s4}
+            cpu_extra["cpu_baseline_config5"] = oracle_config5_solve()
     if rank == 0:
-        print(json.dumps(out), flush=True)
+        # key order: the contract keys, the CPU baselines, the detailed extras, and last the compact
+        # config-3 p-sweep (the metric's p = 1..16 roofline fractions), so a stdout tail keeps it
+        sweep = out.pop("sweep_config3", None)
+        final = dict(out)
+        final.update(cpu_extra)
+        if sweep is not None:
+            final["sweep_config3"] = sweep
+            final["sweep_frac"] = {"p%d" % r["p"]: {"apply": round(r["apply_hbm_frac"], 3),
+                                                    "kernel": round(r["apply_kernel_hbm_frac"], 3),
+                                                    "cheb_step": round(r["cheb_step_hbm_frac"], 3)} for r in sweep}
+        print(json.dumps(final), flush=True)
 
 
 def l2_flush(flush, k, read=True):
