@@ -319,6 +319,21 @@ struct V4Cfg {
   static constexpr int MINB = GS ? MINB_SMEM : (P >= 12 ? 1 : 2);
 };
 
+// Developer timeline (-DSFMG_TIMELINE, tools/v4_timeline.py): %globaltimer marks per block of the
+// v init and the persistent apply; compiled out of the library.
+#ifdef SFMG_TIMELINE
+__device__ unsigned long long g_tl_init[4096 * 2];
+__device__ unsigned long long g_tl_v4[2048 * 4];
+#define TLMARK(arr, stride, cap, s_)                                       \
+  if (threadIdx.x == 0 && blockIdx.x < (cap)) {                            \
+    unsigned long long t_;                                                 \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                 \
+    arr[blockIdx.x * (stride) + (s_)] = t_;                                \
+  }
+#else
+#define TLMARK(arr, stride, cap, s_)
+#endif
+
 // IPS: element-interior nodes (one owner element) take a plain store instead of an fp64 RED (v must be
 // zero there beforehand, as the init kernels leave it).  Used for vectors larger than L2 (N > 2^24)
 // right after the v init, where a RED into a line that the init already evicted costs an HBM read; for
@@ -404,6 +419,7 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
       prefetch_group_l2(grp);
     }
   }
+  TLMARK(g_tl_v4, 4, 2048, 0);
   // wait_mode 2: u is produced by the predecessor; 1: only v is (wait before the first scatter)
   if (wait_mode == 2) pdl_wait();
   bool waited = (wait_mode != 1);
@@ -606,7 +622,9 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
     }
     __syncthreads();
     if (!waited) {
+      TLMARK(g_tl_v4, 4, 2048, 1);
       pdl_wait();
+      TLMARK(g_tl_v4, 4, 2048, 2);
       waited = true;
     }
     if (act) {  // P6: z-line (i=t0, j=t1): v = su + vz, scatter (own column of su)
@@ -624,6 +642,7 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
 #pragma unroll
     for (int k = 0; k < N; ++k) ru[k] = rn[k];
   }
+  TLMARK(g_tl_v4, 4, 2048, 3);
 }
 
 
@@ -854,22 +873,46 @@ __global__ void __launch_bounds__(256) k_init(MeshDev m, int bc, const double* _
   // (the persistent apply) at once, so the apply's launch overlaps this kernel; the apply waits
   // (griddepcontrol.wait) only before its first scatter.  Safe: every init block is already running
   // when the dependent launches, and an init block never waits on anything.
+  TLMARK(g_tl_init, 2, 4096, 0);
   if (early) pdl_trigger();
   const int lane = threadIdx.x & 31;
   const long long rows = (long long)m.My * m.Mz;
   const long long wstride = (long long)gridDim.x * (blockDim.x >> 5);
-  for (long long r = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += wstride) {
+  auto row_bnd = [&](long long r) {
     const unsigned r32 = (unsigned)r;
     const int K = (int)(r32 / (unsigned)m.My), J = (int)(r32 - (unsigned)K * (unsigned)m.My);
-    const bool rowb = (bc == 0) && (J == 0 || J == m.My - 1 || K == m.Kb0 || K == m.Kb1);
+    return (bc == 0) && (J == 0 || J == m.My - 1 || K == m.Kb0 || K == m.Kb1);
+  };
+  // rows, one warp each: Dirichlet rows copied (bnd value), the others zeroed between their two x-face
+  // nodes -- stores only, so a warp never waits on a load in a row it does not own a boundary in
+  for (long long r = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += wstride) {
     double* vr = v + r * m.Mx;
-    const double* ur = u ? u + r * m.Mx : nullptr;
-    for (int I = lane; I < m.Mx; I += 32) {
-      const bool b = rowb || (bc == 0 && (I == 0 || I == m.Mx - 1));
-      vr[I] = b ? (ur ? ur[I] : bval) : 0.0;
+    if (row_bnd(r)) {
+      const double* ur = u ? u + r * m.Mx : nullptr;
+#pragma unroll 4
+      for (int I = lane; I < m.Mx; I += 32) vr[I] = ur ? ur[I] : bval;
+    } else {
+      const int lo = (bc == 0) ? 1 : 0;
+      for (int I = lo + lane; I < m.Mx - lo; I += 32) vr[I] = 0.0;
+    }
+  }
+  // the x-face nodes (I = 0, Mx - 1) of the other rows, one thread per row: the boundary loads of
+  // different rows are independent and overlap
+  if (bc == 0) {
+    const long long tstride = (long long)gridDim.x * blockDim.x;
+    for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += tstride) {
+      if (row_bnd(r)) continue;
+      const long long g0 = r * m.Mx, g1 = g0 + m.Mx - 1;
+      const double a = u ? u[g0] : bval, b = u ? u[g1] : bval;
+      v[g0] = a;
+      v[g1] = b;
     }
   }
   if (!early) pdl_trigger();   // after this block's work (see k_cheb_update)
+#ifdef SFMG_TIMELINE
+  __syncthreads();
+  TLMARK(g_tl_init, 2, 4096, 1);
+#endif
 }
 
 // v = 0 before a p <= 2 standalone apply, whose canonical owner elements store the boundary values
@@ -1563,5 +1606,13 @@ cudaError_t launch_coarse_cg(const MeshDev& m, const double* G, const double* b,
 #ifdef SFMG_KS_DBG
 extern "C" int sfmg_ksdbg_read(unsigned long long* out, int n) {
   return (int)cudaMemcpyFromSymbol(out, sfmg::g_ksdbg, sizeof(unsigned long long) * n);
+}
+#endif
+
+#ifdef SFMG_TIMELINE
+extern "C" int sfmg_tl_read(unsigned long long* init, int ni, unsigned long long* v4, int nv) {
+  cudaError_t e = cudaMemcpyFromSymbol(init, sfmg::g_tl_init, sizeof(unsigned long long) * ni);
+  if (e) return (int)e;
+  return (int)cudaMemcpyFromSymbol(v4, sfmg::g_tl_v4, sizeof(unsigned long long) * nv);
 }
 #endif
