@@ -334,16 +334,189 @@ __device__ unsigned long long g_tl_v4[2048 * 4];
 #define TLMARK(arr, stride, cap, s_)
 #endif
 
+// ------------------------------------------------------------------------------------------
+// FU: the Chebyshev step (or the standalone apply) fused into one persistent kernel for vectors that
+// do not fit in L2 (north_star: "fused with the operator apply so each step makes one pass over HBM";
+// P:936-945 costs a smoother step as one matvec).  y = A x_k is never written to HBM: the blocks RED
+// their element contributions into a ring of `rp` lattice planes (slot = K mod rp, L2 resident, all
+// zero before and after the launch).  The lattice plane set L = planes [L p, (L+1) p) is final once the
+// element layers L - 1 and L are complete; it is cut into gpl contiguous pieces, piece q attached to
+// group slot (L+1) gpl + q + shift, and the block that owns a slot runs its piece right after the
+// slot's scatter: it reads the finished y back from the ring, forms x_{k+1} = x_k + c1 (x_k - x_{k-1}) +
+// c2 D^-1 (b - y) (boundary rows: y = x_k, R4), writes it and re-zeroes the ring entries.  Ordering:
+//  * layer_done[L]: groups of element layer L whose scatter is complete; upd_done[L]: pieces of plane set
+//    L complete.  Both are released by thread 0 (fence + atomic) after the block barrier that follows the
+//    work, at the top of the block's next slot.
+//  * before a slot's scatter, thread 0 acquires upd_done == gpl for every plane set whose ring slots the
+//    element layer's planes reuse, and layer_done == gpl for the layers under the slot's piece.
+// Every wait refers to strictly earlier slots (the launcher bounds shift accordingly) and every block
+// of the persistent grid is resident, so the waits cannot deadlock; each spin still carries a clock
+// timeout that raises *err.
+struct FusedArgs {
+  const double* prev = nullptr;
+  double* out = nullptr;
+  const double* b = nullptr;
+  const double* dinv = nullptr;
+  double c1 = 0.0, c2 = 0.0;
+  unsigned int* layer_done = nullptr;
+  unsigned int* upd_done = nullptr;
+  int* err = nullptr;
+  int rp = 0;      // ring planes
+  int mode = 0;    // 0 Chebyshev / Jacobi update, 1 out = A_D x (ring copied out, boundary rows = x)
+  long long gpl = 0, shift = 0;
+  unsigned chunk = 0, chunk_last = 0;   // nodes per update piece (even), inner plane sets / the last one
+};
+
+// Explicit reductions: in the fused kernel ptxas keeps atomicAdd as the value-returning ATOMG (the
+// scatter then waits a full L2 round trip per node); red.* has no destination register.
+__device__ __forceinline__ void red_add_f64(double* p, double v) {
+  asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(p), "d"(v));
+}
+__device__ __forceinline__ void red_add_u32(unsigned int* p, unsigned v) {
+  asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned int* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __noinline__ void spin_ge(const unsigned int* p, unsigned target, int* err) {
+  if (ld_acquire_u32(p) >= target) return;
+  const long long t0 = clock64();
+  unsigned ns = 100;
+  for (;;) {
+    __nanosleep(ns);   // back-off: hundreds of pollers on one L2 line would stall the releasing atomics
+    if (ns < 1600) ns *= 2;
+    if (ld_acquire_u32(p) >= target) return;
+    // ~2 s: never in a correct run; reported through *err (and every later wait gives up at once)
+    if (clock64() - t0 > (1ll << 32) || *reinterpret_cast<volatile int*>(err)) {
+      atomicExch(err, 86);
+      return;
+    }
+  }
+}
+
+// Node range [lo, hi) of piece q of plane set L (see fused_piece).
+template <int P>
+__device__ __forceinline__ void fused_piece_range(const MeshDev& m, const FusedArgs& f, int L, unsigned q, unsigned& sL,
+                                                  unsigned& eL, unsigned& lo, unsigned& hi) {
+  const unsigned sxy = (unsigned)m.Mx * (unsigned)m.My;
+  const bool last = (L == m.nez - 1);
+  sL = (unsigned)L * P * sxy;
+  eL = last ? (unsigned)m.N : sL + P * sxy;
+  const unsigned chunk = last ? f.chunk_last : f.chunk;
+  lo = (sL & ~1u) + q * chunk;
+  hi = lo + chunk;
+  if (hi > eL) hi = eL;
+}
+// L2 prefetch of the streams a piece reads from HBM (x_{k-1}, b, D^-1), issued by three threads at the top
+// of the slot so that the piece, an element later, finds them in L2.
+template <int P>
+__device__ __forceinline__ void fused_piece_prefetch(const MeshDev& m, const FusedArgs& f, int L, unsigned q, int tid) {
+  if (tid >= 3 || (f.mode & 3) != 0 || (f.mode & 4)) return;
+  const double* src = tid == 0 ? f.b : (tid == 1 ? f.dinv : f.prev);
+  if (tid == 2 && f.c1 == 0.0) return;
+  unsigned sL, eL, lo, hi;
+  fused_piece_range<P>(m, f, L, q, sL, eL, lo, hi);
+  if (lo >= hi) return;
+  lo &= ~1u;                           // 16-byte aligned start, size a multiple of 16 (may touch one node
+  const unsigned n = (hi - lo + 1) & ~1u;   // past the piece; never past the vector's 16-byte padding)
+  unsigned bytes = n * 8;
+  if ((unsigned long long)lo + n > (unsigned long long)m.N) bytes -= 16;
+  if (bytes) bulk_prefetch_l2(src + lo, bytes);
+}
+
+// One update piece of plane set L, by the NT threads of the block (tid = 0..NT-1): nodes
+// [A + q chunk, A + (q+1) chunk) clipped to the set, A = the set's first node rounded down to even, chunk
+// even, so every piece starts on a 16-byte boundary and is walked in double2 pairs (a lone first / last
+// node of an odd-aligned set goes through the scalar path).  The ring already holds y = A_D x including
+// the Dirichlet rows (their owner elements stored x there), so a node needs no lattice coordinates;
+// only its plane (ring slot) is tracked, incrementally from one division per thread.
+template <int P, int NT>
+__device__ __noinline__ void fused_piece(const MeshDev& m, const double* cur, double* ring, const FusedArgs& f,
+                                            int L, unsigned q, int tid) {
+  constexpr int U = 4;
+  const unsigned sxy = (unsigned)m.Mx * (unsigned)m.My;
+  const unsigned rp = (unsigned)f.rp;
+  const bool cheb = ((f.mode & 3) == 0), use_prev = cheb && (f.c1 != 0.0);
+  const double c1 = f.c1, c2 = f.c2;
+  unsigned sL, eL, lo, hi;
+  fused_piece_range<P>(m, f, L, q, sL, eL, lo, hi);
+  if (lo >= hi || (f.mode & 4)) return;   // (mode & 4: developer ablation, no update traffic)
+  auto value = [&](double xc, double xp, double bb, double dd, double y) -> double {
+    return cheb ? xc + c1 * (xc - xp) + c2 * dd * (bb - y) : y;
+  };
+  auto one = [&](unsigned g) {
+    const unsigned K = g / sxy, ri = (K % rp) * sxy + (g - K * sxy);
+    const double y = __ldcg(ring + ri);
+    const double xc = cheb ? __ldcg(cur + g) : 0.0;
+    const double xp = use_prev ? __ldcs(f.prev + g) : 0.0;
+    const double bb = cheb ? __ldcs(f.b + g) : 0.0, dd = cheb ? __ldcs(f.dinv + g) : 0.0;
+    __stcs(f.out + g, value(xc, xp, bb, dd, y));
+    ring[ri] = 0.0;
+  };
+  if (lo < sL) {   // odd-aligned set: its first node alone
+    if (tid == 0) one(sL);
+    lo += 2;
+  }
+  if (hi & 1) {    // (only hi == eL can be odd)
+    --hi;
+    if (tid == NT - 1) one(hi);
+  }
+  if (lo >= hi) return;
+  const unsigned np = (hi - lo) >> 1;
+  const unsigned K0 = lo / sxy, rr0 = lo - K0 * sxy, slot0 = K0 % rp;
+  for (unsigned i0 = 0; i0 < np; i0 += NT * U) {
+    double2 xc[U], xp[U], bb[U], dd[U];
+    double y0[U], y1[U];
+    unsigned a0[U], a1[U];
+#pragma unroll
+    for (int w = 0; w < U; ++w) {
+      const unsigned i = i0 + w * NT + tid;
+      xc[w] = xp[w] = bb[w] = dd[w] = make_double2(0.0, 0.0);
+      if (i < np) {
+        const unsigned g = lo + 2 * i;
+        unsigned r = rr0 + 2 * i, slot = slot0;
+        while (r >= sxy) { r -= sxy; slot = (slot + 1 == rp) ? 0 : slot + 1; }
+        a0[w] = slot * sxy + r;
+        a1[w] = (r + 1 < sxy) ? a0[w] + 1 : ((slot + 1 == rp) ? 0 : slot + 1) * sxy;
+        y0[w] = __ldcg(ring + a0[w]);
+        y1[w] = __ldcg(ring + a1[w]);
+        if (cheb) {
+          xc[w] = __ldcg(reinterpret_cast<const double2*>(cur + g));
+          if (use_prev) xp[w] = __ldcs(reinterpret_cast<const double2*>(f.prev + g));
+          bb[w] = __ldcs(reinterpret_cast<const double2*>(f.b + g));
+          dd[w] = __ldcs(reinterpret_cast<const double2*>(f.dinv + g));
+        }
+      }
+    }
+#pragma unroll
+    for (int w = 0; w < U; ++w) {
+      const unsigned i = i0 + w * NT + tid;
+      if (i < np) {
+        double2 o;
+        o.x = value(xc[w].x, xp[w].x, bb[w].x, dd[w].x, y0[w]);
+        o.y = value(xc[w].y, xp[w].y, bb[w].y, dd[w].y, y1[w]);
+        __stcs(reinterpret_cast<double2*>(f.out + lo + 2 * i), o);
+        ring[a0[w]] = 0.0;
+        ring[a1[w]] = 0.0;
+      }
+    }
+  }
+}
+
 // IPS: element-interior nodes (one owner element) take a plain store instead of an fp64 RED (v must be
 // zero there beforehand, as the init kernels leave it).  Used for vectors larger than L2 (N > 2^24)
 // right after the v init, where a RED into a line that the init already evicted costs an HBM read; for
 // L2-resident vectors the REDs are cheaper (config 2 measured slower with plain stores).
-template <int P, bool DIR, bool GS, bool IPS = false>
+template <int P, bool DIR, bool GS, bool IPS = false, bool FU = false>
 __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
     k_apply_v4(MeshDev m, const double* __restrict__ G, const double* __restrict__ u, double* __restrict__ v,
-               long long ngroups, int wait_mode, int write_bnd) {
+               long long ngroups, int wait_mode, int write_bnd, FusedArgs f) {
   using C = V4Cfg<P, GS>;
   constexpr int N = C::N, N2 = C::N2, N3 = C::N3;
+  auto bsync = [&]() { __syncthreads(); };
   constexpr bool EO = (P % 2 == 0) && P >= 4;   // even-odd line products
   // the next group's u column is loaded right after this group's is staged, so it is in flight
   // during the whole element (measured: p = 16 -2.5 %, p <= 8 within noise)
@@ -362,6 +535,7 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
   double* s0 = smem + (GS ? C::EPB * 6 * N3 : 0) + le * 2 * N3;   // per element: s0, su
   double* su = s0 + N3;
   uint64_t* bar = (uint64_t*)(smem + C::EPB * (GS ? 8 : 2) * N3);
+  if constexpr (FU) static_assert(DIR && GS && !IPS, "fused step: Dirichlet operator, staged factors");
   const double* gE = sG + le * 6 * N3;
   const long long sxy = (long long)m.Mx * m.My;
   const long long gstride = gridDim.x;
@@ -427,8 +601,22 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
   if (grp < ngroups) load_column(grp, ru);
   if (grp + gstride < ngroups) prefetch_column(grp + gstride);
   unsigned phase = 0;
+  // FU: this block's finished but unpublished work: acc_ln groups of element layer acc_layer and acc_sn
+  // pieces of plane set acc_set.  They are released (one fence, then the counter REDs) when the block moves
+  // on to another layer / set -- the counters only matter once a layer / set is complete, and a fence per
+  // slot costs ~1 us of the block's critical path.
+  int acc_layer = -1, acc_ln = 0, acc_set = -1, acc_sn = 0;
+  int lay_chk = -1;     // FU: element layers <= lay_chk are known to be complete
+  int chk_layer = -1;   // FU: plane sets <= chk_layer are known to be updated (their ring slots re-zeroed)
   for (; grp < ngroups; grp += gstride) {
     constexpr int zero = 0;
+    if constexpr (FU) {   // this slot's update piece: start its HBM streams towards L2 now
+      const long long pjp = grp - f.gpl - f.shift;
+      if (pjp >= 0 && threadIdx.x < 3 && !(f.mode & 8)) {
+        const int Lp = (int)((unsigned)pjp / (unsigned)f.gpl);
+        fused_piece_prefetch<P>(m, f, Lp, (unsigned)pjp - (unsigned)Lp * (unsigned)f.gpl, threadIdx.x);
+      }
+    }
     // last group of this block: let a programmatic dependent (the Chebyshev update) launch now; it
     // waits (griddepcontrol.wait) for this grid's completion before reading v.  Small vectors only
     // (config 4 measured 2.51 -> 2.61 ms with it)
@@ -467,7 +655,7 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
       load_column(grp + gstride, rn);
       if (grp + 2 * gstride < ngroups) prefetch_column(grp + 2 * gstride);
     }
-    __syncthreads();
+    bsync();
     {  // P1: g0 on x-line (j=t0, k=t1) -> s0 (TR: in place)
       double L[N];
 #pragma unroll
@@ -487,7 +675,7 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
         }
       }
     }
-    __syncthreads();
+    bsync();
     {  // P2: g1 on y-line (i=t0, k=t1), in place in su
       // y-line element j of line (i, k): natural su[i + n j + n^2 k], transposed su[j + n i + n^2 k]
       const int yb = TR ? N * t0 + N2 * t1 : t0 + N2 * t1;
@@ -510,7 +698,7 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
         }
       }
     }
-    __syncthreads();
+    bsync();
     if (GS) {
       mbar_wait(bar, phase);
       phase ^= 1u;
@@ -563,7 +751,7 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
         }
       }
     }
-    __syncthreads();
+    bsync();
     {  // factors consumed: next group's G (TMA from L2) and the L2 prefetch of the group after
       const long long nx = grp + gstride;
       if (nx < ngroups && threadIdx.x == 0) {
@@ -598,7 +786,7 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
         }
       }
     }
-    __syncthreads();
+    bsync();
     {  // P5: su = D^T w1 + v0 on y-line (i=t0, k=t1) (TR: su = Y in place; v0 is added in P6)
       const int yb = TR ? N * t0 + N2 * t1 : t0 + N2 * t1;
       constexpr int ys = TR ? 1 : N;
@@ -620,7 +808,31 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
         }
       }
     }
-    __syncthreads();
+    // FU: the update piece attached to this group slot (plane set one or more layers behind)
+    const long long pj = (FU && !(f.mode & 512)) ? grp - f.gpl - f.shift : -1;
+    if constexpr (FU) {
+      const int cur_set = pj >= 0 ? (int)((unsigned)pj / (unsigned)f.gpl) : -1;
+      const bool fl = acc_ln > 0 && acc_layer != ez, fs = acc_sn > 0 && acc_set != cur_set;
+      if (threadIdx.x == 0) {
+        // release the finished layer / set of the earlier slots (every thread passed block barriers since
+        // their last RED / store)
+        if (fl || fs) {
+          fence_acq_rel_gpu();
+          if (fl) red_add_u32(f.layer_done + acc_layer, (unsigned)acc_ln);
+          if (fs) red_add_u32(f.upd_done + acc_set, (unsigned)acc_sn);
+        }
+        // plane sets whose ring slots this element layer's planes [ez p, (ez+1) p] reuse must be updated
+        const int need = (ez * P + P - f.rp >= 0) ? (ez * P + P - f.rp) / P : -1;
+        for (; chk_layer < need && !(f.mode & 32); ++chk_layer)
+          spin_ge(f.upd_done + chk_layer + 1, (unsigned)f.gpl, f.err);
+        // the piece's plane set is final once the element layers up to it are complete
+        for (; lay_chk < cur_set && !(f.mode & 32); ++lay_chk)
+          spin_ge(f.layer_done + lay_chk + 1, (unsigned)f.gpl, f.err);
+      }
+      if (fl) acc_ln = 0;
+      if (fs) acc_sn = 0;
+    }
+    bsync();
     if (!waited) {
       TLMARK(g_tl_v4, 4, 2048, 1);
       pdl_wait();
@@ -629,18 +841,63 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
     }
     if (act) {  // P6: z-line (i=t0, j=t1): v = su + vz, scatter (own column of su)
       const bool own_xy = (t0 > 0 || ex == 0) && (t1 > 0 || ey == 0);
+      const long long gxy = (long long)(ex * P + t0) + (long long)m.Mx * (ey * P + t1);
+      const int kz0 = FU ? (ez * P) % f.rp : 0;   // ring slot of the element's bottom plane
 #pragma unroll
       for (int c = 0; c < N; ++c) {
         bool bnd = false;
         if (DIR) { const int K = ez * P + c; bnd = bxy || K == m.Kb0 || K == m.Kb1; }
         const double xy = TR ? s0[t + N2 * c] + su[t1 + N * t0 + N2 * c] : su[t + N2 * c];
-        if (IPS && t0 > 0 && t0 < P && t1 > 0 && t1 < P && c > 0 && c < P) v[gcol + sxy * c] = xy + vz[c];
+        if constexpr (FU) {
+          int slot = kz0 + c;
+          if (slot >= f.rp) slot -= f.rp;
+          if (f.mode & 256) {   // developer ablation: the whole y vector instead of the ring
+            slot = ez * P + c;
+            if (gxy + sxy * slot >= m.N - 1024) continue;   // (the counters sit there in this mode)
+          }
+          if (!bnd) red_add_f64(v + gxy + sxy * slot, xy + vz[c]);
+          else if (own_xy && (c > 0 || ez == 0)) v[gxy + sxy * slot] = u[gcol + sxy * c];   // A_D x = x (R4)
+        } else if (IPS && t0 > 0 && t0 < P && t1 > 0 && t1 < P && c > 0 && c < P) v[gcol + sxy * c] = xy + vz[c];
         else if (!bnd) atomicAdd(v + gcol + sxy * c, xy + vz[c]);
         else if (write_bnd && own_xy && (c > 0 || ez == 0)) v[gcol + sxy * c] = u[gcol + sxy * c];  // (I-M) u
       }
     }
 #pragma unroll
     for (int k = 0; k < N; ++k) ru[k] = rn[k];
+    if constexpr (FU) {
+      acc_layer = ez;   // (all elements of a group lie in one layer: checked by the launcher)
+      ++acc_ln;
+      if (pj >= 0) {
+        acc_set = (int)((unsigned)pj / (unsigned)f.gpl);
+        ++acc_sn;
+        fused_piece<P, C::THREADS>(m, u, v, f, acc_set, (unsigned)pj - (unsigned)acc_set * (unsigned)f.gpl, threadIdx.x);
+      }
+    }
+  }
+  if constexpr (FU) {   // the update pieces attached to the slots after the last element group
+    const long long npieces = (f.mode & 512) ? 0 : (long long)m.nez * f.gpl;
+    for (;; grp += gstride) {
+      const long long pj = grp - f.gpl - f.shift;
+      const int cur_set = (pj >= 0 && pj < npieces) ? (int)((unsigned)pj / (unsigned)f.gpl) : -1;
+      const bool fl = acc_ln > 0, fs = acc_sn > 0 && acc_set != cur_set;
+      bsync();
+      if (threadIdx.x == 0 && (fl || fs)) {
+        fence_acq_rel_gpu();
+        if (fl) red_add_u32(f.layer_done + acc_layer, (unsigned)acc_ln);
+        if (fs) red_add_u32(f.upd_done + acc_set, (unsigned)acc_sn);
+      }
+      acc_ln = 0;
+      if (fs) acc_sn = 0;
+      if (pj >= npieces) break;
+      if (pj < 0) continue;
+      if (threadIdx.x == 0) {
+        for (; lay_chk < cur_set; ++lay_chk) spin_ge(f.layer_done + lay_chk + 1, (unsigned)f.gpl, f.err);
+      }
+      bsync();
+      acc_set = cur_set;
+      ++acc_sn;
+      fused_piece<P, C::THREADS>(m, u, v, f, cur_set, (unsigned)pj - (unsigned)cur_set * (unsigned)f.gpl, threadIdx.x);
+    }
   }
   TLMARK(g_tl_v4, 4, 2048, 3);
 }
@@ -1333,10 +1590,10 @@ static cudaError_t apply_pd(const MeshDev& m, const double* G, const double* u, 
       int r2 = 0;
       if ((e = persistent_blocks(occ_ips, k_apply_v4<P, DIR, GS, true>, C::THREADS, C::SMEM, r2))) return e;
       return launch_pdl(k_apply_v4<P, DIR, GS, true>, (unsigned)grid, (unsigned)C::THREADS, C::SMEM, s, mm, G, u, v,
-                        groups, wait_mode, write_bnd);
+                        groups, wait_mode, write_bnd, FusedArgs{});
     }
     return launch_pdl(k_apply_v4<P, DIR, GS>, (unsigned)grid, (unsigned)C::THREADS, C::SMEM, s, mm, G, u, v, groups,
-                      wait_mode, write_bnd);
+                      wait_mode, write_bnd, FusedArgs{});
   }
 }
 template <int P>
@@ -1353,6 +1610,123 @@ cudaError_t launch_apply(const MeshDev& m, int bc, const double* G, const double
   SFMG_DISPATCH_P(m.p, apply_p, m, bc, G, u, v, wait_mode, write_bnd, s, &err);
   if (err) return err;
   return cudaGetLastError();
+}
+
+// ---- fused Chebyshev step / apply for vectors beyond L2 (k_apply_v4<.., FU>)
+
+// SFMG_FUSED: 0 never, 1 wherever the kernel applies (tests), unset: vectors of more than 2^24 dofs
+static int fused_env() {
+  static const int v = [] {
+    const char* e = getenv("SFMG_FUSED");
+    return e ? atoi(e) : -1;
+  }();
+  return v;
+}
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+template <int P>
+static constexpr int fused_epb() {
+  if constexpr (P >= 3 && P <= 8) return V4Cfg<P, true>::EPB;
+  return 0;
+}
+static int fused_epb_of(int p) {
+  switch (p) {
+    case 3: return fused_epb<3>();
+    case 4: return fused_epb<4>();
+    case 5: return fused_epb<5>();
+    case 6: return fused_epb<6>();
+    case 7: return fused_epb<7>();
+    case 8: return fused_epb<8>();
+  }
+  return 0;
+}
+static int fused_ring_planes(const MeshDev& m) {
+  static const int extra = env_int("SFMG_FUSED_RING_EXTRA", 0);
+  int rp = 3 * m.p + 1 + extra;   // >= 3 p + 1: the pieces may lag their layer by a grid round (launcher)
+  if (rp < 2 * m.p + 1) rp = 2 * m.p + 1;
+  return rp > m.Mz ? m.Mz : rp;
+}
+size_t fused_scratch_doubles(const MeshDev& m) {
+  return (size_t)fused_ring_planes(m) * m.Mx * m.My + (size_t)m.nez + 8;   // ring, counters (2 nez + 1 ints)
+}
+bool fused_available(const MeshDev& m) {
+  const int mode = fused_env();
+  if (mode == 0 || m.dim != 3 || m.quad) return false;
+  const int epb = fused_epb_of(m.p);
+  if (epb == 0 || m.nez < 3) return false;
+  if (((long long)m.nex * m.ney) % epb) return false;       // every group inside one element layer
+  if (m.N >= (1ll << 32)) return false;                      // 32-bit lattice arithmetic in the updater
+  if (fused_scratch_doubles(m) > (size_t)m.N) return false;  // the ring lives in the level's y vector
+  if (2 * m.p + 1 > m.Mz) return false;
+  return mode == 1 || m.N > kEarlyMaxN;
+}
+
+template <int P>
+static void fused_p(const MeshDev& m, const double* G, const double* cur, double* scratch, FusedArgs f,
+                    cudaStream_t s, cudaError_t* err) {
+  if constexpr (P >= 3 && P <= 8) {
+    using C = V4Cfg<P, true>;
+    auto kern = k_apply_v4<P, true, true, false, true>;
+    static IntPerDevice occ;
+    int resident = 0;
+    if ((*err = persistent_blocks(occ, kern, C::THREADS, C::SMEM, resident))) return;
+    const long long groups = m.E / C::EPB;
+    long long grid = (long long)resident * num_sms();
+    if (grid > groups) grid = groups;
+    f.gpl = ((long long)m.nex * m.ney) / C::EPB;
+    auto even_chunk = [&](long long nodes) {   // ceil((nodes + 1) / gpl), rounded up to even
+      long long c = (nodes + 1 + f.gpl - 1) / f.gpl;
+      return (unsigned)((c + 1) & ~1ll);
+    };
+    const long long sxy = (long long)m.Mx * m.My;
+    f.chunk = even_chunk((long long)P * sxy);
+    f.chunk_last = even_chunk((long long)(P + 1) * sxy);
+    // A piece runs after its slot's scatter, and a scatter waits for the plane sets whose ring slots it
+    // reuses (sets <= M + 1 - ceil(rp / p) for element layer M); those must be attached to earlier
+    // slots: shift <= (ceil(rp / p) - 3) gpl.  rp = 2 p + 1 allows no shift, rp >= 3 p + 1 one grid round.
+    static const int shift_rounds = env_int("SFMG_FUSED_SHIFT", 1);
+    const long long max_shift = (long long)((f.rp + P - 1) / P - 3) * f.gpl;
+    f.shift = grid * shift_rounds;
+    if (f.shift > max_shift) f.shift = max_shift;
+    if (f.shift < 0) f.shift = 0;
+    MeshDev mm = m;
+    mm.pdl_early = 0;
+    if (f.mode & 64) fprintf(stderr, "fused p=%d resident=%d grid=%lld gpl=%lld rp=%d shift=%lld\n", P, resident, grid, f.gpl, f.rp, f.shift);
+    // plain launch (no programmatic overlap): every block is resident and nothing of the previous step
+    // is still running when the first spin-wait starts
+    kern<<<(unsigned)grid, C::THREADS, C::SMEM, s>>>(mm, G, cur, scratch, groups, 0, 0, f);
+    *err = cudaGetLastError();
+  } else {
+    *err = cudaErrorInvalidValue;
+  }
+}
+
+// One fused step on the whole lattice: mode 0 out = cur + c1 (cur - prev) + c2 dinv (b - A_D cur);
+// mode 1 out = A_D cur.  scratch: fused_scratch_doubles(m) doubles whose ring part is all zero (it is
+// left all zero).  All vectors 16-byte aligned; out may alias prev or cur.
+cudaError_t launch_fused_step(const MeshDev& m, const double* G, const double* cur, const double* prev, double* out,
+                              const double* b, const double* dinv, double* scratch, double c1, double c2, int mode,
+                              cudaStream_t s) {
+  FusedArgs f;
+  f.prev = prev; f.out = out; f.b = b; f.dinv = dinv; f.c1 = c1; f.c2 = c2; f.mode = mode;
+  f.rp = fused_ring_planes(m);
+  const size_t ring = (size_t)f.rp * m.Mx * m.My;
+  static const int dbg = env_int("SFMG_FUSED_DBG", 0);
+  f.mode |= dbg;
+  unsigned int* cnt = reinterpret_cast<unsigned int*>((f.mode & 256) ? scratch + m.N - 1024 : scratch + ring);
+  f.layer_done = cnt;
+  f.upd_done = cnt + m.nez;
+  f.err = reinterpret_cast<int*>(cnt + 2 * m.nez);
+  cudaError_t e = cudaMemsetAsync(cnt, 0, sizeof(unsigned int) * (2 * (size_t)m.nez + 1), s);
+  if (e) return e;
+  cudaError_t err = cudaSuccess;
+  SFMG_DISPATCH_P(m.p, fused_p, m, G, cur, scratch, f, s, &err);
+  return err;
+}
+cudaError_t fused_zero_ring(const MeshDev& m, double* scratch, cudaStream_t s) {
+  return cudaMemsetAsync(scratch, 0, sizeof(double) * fused_scratch_doubles(m), s);
 }
 
 template <int P>

@@ -162,8 +162,16 @@ static cudaError_t element_kernel(sfmg_level_s* lv, int bc, const double* u, dou
   return cudaEventRecord(b, s);
 }
 
+static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
+
 static cudaError_t op_apply(sfmg_level_s* lv, int bc, const double* u, double* v, cudaStream_t s) {
   cudaError_t e;
+  // vectors beyond L2: one fused kernel, A_D u accumulated in an L2-resident plane ring inside lv->y and
+  // copied out one element layer behind (no v init, no RED traffic to HBM)
+  if (bc == 0 && v != lv->y && u != lv->y && !lv->prof && fused_available(lv->m) && aligned16(u) && aligned16(v)) {
+    if ((e = fused_zero_ring(lv->m, lv->y, s))) return e;
+    return launch_fused_step(lv->m, lv->G, u, nullptr, v, nullptr, nullptr, lv->y, 0.0, 0.0, 1, s);
+  }
   if (lv->p <= 2 && !lv->m.quad && lv->m.dim == 3) {   // zero v, then the thread-per-element kernel, whose
                                                        // canonical owner elements store (I - M) u
     if ((e = launch_zero(v, lv->N, s))) return e;
@@ -182,7 +190,8 @@ static cudaError_t op_cheb(sfmg_level_s* lv, const double* b, double* x, int K, 
                            cudaStream_t s) {
   const double theta = 0.5 * (hi + lo), delta = 0.5 * (hi - lo), sigma = theta / delta;
   double rho_prev = 1.0 / sigma;
-  cudaError_t e = op_apply(lv, 0, x, lv->y, s);
+  const bool fused = !lv->prof && fused_available(lv->m) && aligned16(b) && aligned16(x) && b != lv->y && x != lv->y;
+  cudaError_t e = fused ? fused_zero_ring(lv->m, lv->y, s) : op_apply(lv, 0, x, lv->y, s);
   if (e) return e;
   double* A = x;
   double* B = lv->t0;
@@ -197,6 +206,13 @@ static cudaError_t op_cheb(sfmg_level_s* lv, const double* b, double* x, int K, 
       rho_prev = rho;
     }
     double* out = (k == K - 1) ? A : (k == 0 ? B : prev);
+    if (fused) {   // one kernel per step: apply + recurrence, y = A_D x_k never leaves L2
+      e = launch_fused_step(lv->m, lv->G, cur, prev ? prev : cur, out, b, lv->dinv, lv->y, c1, c2, 0, s);
+      if (e) return e;
+      prev = cur;
+      cur = out;
+      continue;
+    }
     if (k > 0) {
       e = element_kernel(lv, 0, cur, lv->y, 2, 0, s);   // y was re-initialised by the last update
       if (e) return e;
@@ -213,6 +229,12 @@ static cudaError_t op_cheb(sfmg_level_s* lv, const double* b, double* x, int K, 
 // Chebyshev update kernel with c1 = 0, c2 = omega (it also re-initialises y for the next apply).
 static cudaError_t op_jacobi(sfmg_level_s* lv, const double* b, double* x, int steps, double omega,
                              cudaStream_t s) {
+  if (!lv->prof && fused_available(lv->m) && aligned16(b) && aligned16(x) && b != lv->y && x != lv->y) {
+    cudaError_t e = fused_zero_ring(lv->m, lv->y, s);
+    for (int k = 0; k < steps && !e; ++k)
+      e = launch_fused_step(lv->m, lv->G, x, x, x, b, lv->dinv, lv->y, 0.0, omega, 0, s);
+    return e;
+  }
   for (int k = 0; k < steps; ++k) {
     cudaError_t e = (k == 0) ? op_apply(lv, 0, x, lv->y, s) : element_kernel(lv, 0, x, lv->y, 2, 0, s);
     if (e) return e;

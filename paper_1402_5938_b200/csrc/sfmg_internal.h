@@ -183,6 +183,17 @@ cudaError_t launch_load(const MeshDev& m, int rhs_id, double* f, cudaStream_t s)
 cudaError_t launch_cheb_update(const MeshDev& m, const double* cur, const double* prev, double* out,
                                const double* b, double* y, const double* dinv, double c1, double c2,
                                cudaStream_t s);
+// Fused step for vectors beyond L2 (k_apply_v4<.., FU>, 3 <= p <= 8, bc 0): one persistent kernel forms
+// y = A_D cur in an L2-resident ring of lattice planes and, one element layer behind, mode 0:
+// out = cur + c1 (cur - prev) + c2 dinv (b - y) (prev unused when c1 == 0); mode 1: out = y.
+// scratch: fused_scratch_doubles(m) doubles, ring part all zero on entry (fused_zero_ring) and on exit.
+// Vectors 16-byte aligned; out may alias prev or cur.
+bool fused_available(const MeshDev& m);
+size_t fused_scratch_doubles(const MeshDev& m);
+cudaError_t fused_zero_ring(const MeshDev& m, double* scratch, cudaStream_t s);
+cudaError_t launch_fused_step(const MeshDev& m, const double* G, const double* cur, const double* prev, double* out,
+                              const double* b, const double* dinv, double* scratch, double c1, double c2, int mode,
+                              cudaStream_t s);
 cudaError_t launch_export_geometry(const MeshDev& m, const double* G, double* out, cudaStream_t s);
 // elements for which G storage is allocated (p <= 2: rounded up to 32 for the interleaved layout)
 long long geometry_elems(int p, long long E);
