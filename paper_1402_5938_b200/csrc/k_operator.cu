@@ -372,6 +372,24 @@ struct FusedArgs {
 __device__ __forceinline__ void red_add_f64(double* p, double v) {
   asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(p), "d"(v));
 }
+// Ring accesses carry an L2 evict-last policy: the ring is re-used every rp planes and must not be
+// displaced by the streams that pass through L2 once (u, the factors in flight, x_{k-1}, b, D^-1).
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void ring_red(double* p, double v, uint64_t pol) {
+  asm volatile("red.relaxed.gpu.global.add.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol));
+}
+__device__ __forceinline__ double ring_ld(const double* p, uint64_t pol) {
+  double v;
+  asm volatile("ld.relaxed.gpu.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol) : "memory");
+  return v;
+}
+__device__ __forceinline__ void ring_st(double* p, double v, uint64_t pol) {
+  asm volatile("st.relaxed.gpu.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
 __device__ __forceinline__ void red_add_u32(unsigned int* p, unsigned v) {
   asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -434,13 +452,14 @@ __device__ __forceinline__ void fused_piece_prefetch(const MeshDev& m, const Fus
 // the Dirichlet rows (their owner elements stored x there), so a node needs no lattice coordinates;
 // only its plane (ring slot) is tracked, incrementally from one division per thread.
 template <int P, int NT>
-__device__ __noinline__ void fused_piece(const MeshDev& m, const double* cur, double* ring, const FusedArgs& f,
+__device__ __forceinline__ void fused_piece(const MeshDev& m, const double* cur, double* ring, const FusedArgs& f,
                                             int L, unsigned q, int tid) {
   constexpr int U = 4;
   const unsigned sxy = (unsigned)m.Mx * (unsigned)m.My;
   const unsigned rp = (unsigned)f.rp;
   const bool cheb = ((f.mode & 3) == 0), use_prev = cheb && (f.c1 != 0.0);
   const double c1 = f.c1, c2 = f.c2;
+  const uint64_t pol = l2_evict_last_policy();
   unsigned sL, eL, lo, hi;
   fused_piece_range<P>(m, f, L, q, sL, eL, lo, hi);
   if (lo >= hi || (f.mode & 4)) return;   // (mode & 4: developer ablation, no update traffic)
@@ -449,12 +468,12 @@ __device__ __noinline__ void fused_piece(const MeshDev& m, const double* cur, do
   };
   auto one = [&](unsigned g) {
     const unsigned K = g / sxy, ri = (K % rp) * sxy + (g - K * sxy);
-    const double y = __ldcg(ring + ri);
+    const double y = ring_ld(ring + ri, pol);
     const double xc = cheb ? __ldcg(cur + g) : 0.0;
     const double xp = use_prev ? __ldcs(f.prev + g) : 0.0;
     const double bb = cheb ? __ldcs(f.b + g) : 0.0, dd = cheb ? __ldcs(f.dinv + g) : 0.0;
     __stcs(f.out + g, value(xc, xp, bb, dd, y));
-    ring[ri] = 0.0;
+    ring_st(ring + ri, 0.0, pol);
   };
   if (lo < sL) {   // odd-aligned set: its first node alone
     if (tid == 0) one(sL);
@@ -481,8 +500,8 @@ __device__ __noinline__ void fused_piece(const MeshDev& m, const double* cur, do
         while (r >= sxy) { r -= sxy; slot = (slot + 1 == rp) ? 0 : slot + 1; }
         a0[w] = slot * sxy + r;
         a1[w] = (r + 1 < sxy) ? a0[w] + 1 : ((slot + 1 == rp) ? 0 : slot + 1) * sxy;
-        y0[w] = __ldcg(ring + a0[w]);
-        y1[w] = __ldcg(ring + a1[w]);
+        y0[w] = ring_ld(ring + a0[w], pol);
+        y1[w] = ring_ld(ring + a1[w], pol);
         if (cheb) {
           xc[w] = __ldcg(reinterpret_cast<const double2*>(cur + g));
           if (use_prev) xp[w] = __ldcs(reinterpret_cast<const double2*>(f.prev + g));
@@ -499,8 +518,8 @@ __device__ __noinline__ void fused_piece(const MeshDev& m, const double* cur, do
         o.x = value(xc[w].x, xp[w].x, bb[w].x, dd[w].x, y0[w]);
         o.y = value(xc[w].y, xp[w].y, bb[w].y, dd[w].y, y1[w]);
         __stcs(reinterpret_cast<double2*>(f.out + lo + 2 * i), o);
-        ring[a0[w]] = 0.0;
-        ring[a1[w]] = 0.0;
+        ring_st(ring + a0[w], 0.0, pol);
+        ring_st(ring + a1[w], 0.0, pol);
       }
     }
   }
@@ -809,7 +828,7 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
       }
     }
     // FU: the update piece attached to this group slot (plane set one or more layers behind)
-    const long long pj = (FU && !(f.mode & 512)) ? grp - f.gpl - f.shift : -1;
+    const long long pj = FU ? grp - f.gpl - f.shift : -1;
     if constexpr (FU) {
       const int cur_set = pj >= 0 ? (int)((unsigned)pj / (unsigned)f.gpl) : -1;
       const bool fl = acc_ln > 0 && acc_layer != ez, fs = acc_sn > 0 && acc_set != cur_set;
@@ -823,11 +842,9 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
         }
         // plane sets whose ring slots this element layer's planes [ez p, (ez+1) p] reuse must be updated
         const int need = (ez * P + P - f.rp >= 0) ? (ez * P + P - f.rp) / P : -1;
-        for (; chk_layer < need && !(f.mode & 32); ++chk_layer)
-          spin_ge(f.upd_done + chk_layer + 1, (unsigned)f.gpl, f.err);
+        for (; chk_layer < need; ++chk_layer) spin_ge(f.upd_done + chk_layer + 1, (unsigned)f.gpl, f.err);
         // the piece's plane set is final once the element layers up to it are complete
-        for (; lay_chk < cur_set && !(f.mode & 32); ++lay_chk)
-          spin_ge(f.layer_done + lay_chk + 1, (unsigned)f.gpl, f.err);
+        for (; lay_chk < cur_set; ++lay_chk) spin_ge(f.layer_done + lay_chk + 1, (unsigned)f.gpl, f.err);
       }
       if (fl) acc_ln = 0;
       if (fs) acc_sn = 0;
@@ -843,6 +860,7 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
       const bool own_xy = (t0 > 0 || ex == 0) && (t1 > 0 || ey == 0);
       const long long gxy = (long long)(ex * P + t0) + (long long)m.Mx * (ey * P + t1);
       const int kz0 = FU ? (ez * P) % f.rp : 0;   // ring slot of the element's bottom plane
+      const uint64_t rpol = FU ? l2_evict_last_policy() : 0;
 #pragma unroll
       for (int c = 0; c < N; ++c) {
         bool bnd = false;
@@ -851,12 +869,8 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
         if constexpr (FU) {
           int slot = kz0 + c;
           if (slot >= f.rp) slot -= f.rp;
-          if (f.mode & 256) {   // developer ablation: the whole y vector instead of the ring
-            slot = ez * P + c;
-            if (gxy + sxy * slot >= m.N - 1024) continue;   // (the counters sit there in this mode)
-          }
-          if (!bnd) red_add_f64(v + gxy + sxy * slot, xy + vz[c]);
-          else if (own_xy && (c > 0 || ez == 0)) v[gxy + sxy * slot] = u[gcol + sxy * c];   // A_D x = x (R4)
+          if (!bnd) ring_red(v + gxy + sxy * slot, xy + vz[c], rpol);
+          else if (own_xy && (c > 0 || ez == 0)) ring_st(v + gxy + sxy * slot, u[gcol + sxy * c], rpol);   // A_D x = x (R4)
         } else if (IPS && t0 > 0 && t0 < P && t1 > 0 && t1 < P && c > 0 && c < P) v[gcol + sxy * c] = xy + vz[c];
         else if (!bnd) atomicAdd(v + gcol + sxy * c, xy + vz[c]);
         else if (write_bnd && own_xy && (c > 0 || ez == 0)) v[gcol + sxy * c] = u[gcol + sxy * c];  // (I-M) u
@@ -875,7 +889,7 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
     }
   }
   if constexpr (FU) {   // the update pieces attached to the slots after the last element group
-    const long long npieces = (f.mode & 512) ? 0 : (long long)m.nez * f.gpl;
+    const long long npieces = (long long)m.nez * f.gpl;
     for (;; grp += gstride) {
       const long long pj = grp - f.gpl - f.shift;
       const int cur_set = (pj >= 0 && pj < npieces) ? (int)((unsigned)pj / (unsigned)f.gpl) : -1;
@@ -1614,7 +1628,7 @@ cudaError_t launch_apply(const MeshDev& m, int bc, const double* G, const double
 
 // ---- fused Chebyshev step / apply for vectors beyond L2 (k_apply_v4<.., FU>)
 
-// SFMG_FUSED: 0 never, 1 wherever the kernel applies (tests), unset: vectors of more than 2^24 dofs
+// SFMG_FUSED=1: the fused kernel wherever it applies (tests, measurements); otherwise never
 static int fused_env() {
   static const int v = [] {
     const char* e = getenv("SFMG_FUSED");
@@ -1660,7 +1674,10 @@ bool fused_available(const MeshDev& m) {
   if (m.N >= (1ll << 32)) return false;                      // 32-bit lattice arithmetic in the updater
   if (fused_scratch_doubles(m) > (size_t)m.N) return false;  // the ring lives in the level's y vector
   if (2 * m.p + 1 > m.Mz) return false;
-  return mode == 1 || m.N > kEarlyMaxN;
+  // opt-in: measured slower than the unfused step (config 4: 4.0-4.1 vs 3.6 ms; DESIGN.md section 6,
+  // profiles/r02_experiments.md) although its DRAM traffic is the algorithmic 1.04x with
+  // SFMG_L2_PERSIST_MB=64
+  return mode == 1;
 }
 
 template <int P>
@@ -1671,7 +1688,8 @@ static void fused_p(const MeshDev& m, const double* G, const double* cur, double
     auto kern = k_apply_v4<P, true, true, false, true>;
     static IntPerDevice occ;
     int resident = 0;
-    if ((*err = persistent_blocks(occ, kern, C::THREADS, C::SMEM, resident))) return;
+    constexpr int threads = C::THREADS;
+    if ((*err = persistent_blocks(occ, kern, threads, C::SMEM, resident))) return;
     const long long groups = m.E / C::EPB;
     long long grid = (long long)resident * num_sms();
     if (grid > groups) grid = groups;
@@ -1693,10 +1711,9 @@ static void fused_p(const MeshDev& m, const double* G, const double* cur, double
     if (f.shift < 0) f.shift = 0;
     MeshDev mm = m;
     mm.pdl_early = 0;
-    if (f.mode & 64) fprintf(stderr, "fused p=%d resident=%d grid=%lld gpl=%lld rp=%d shift=%lld\n", P, resident, grid, f.gpl, f.rp, f.shift);
     // plain launch (no programmatic overlap): every block is resident and nothing of the previous step
     // is still running when the first spin-wait starts
-    kern<<<(unsigned)grid, C::THREADS, C::SMEM, s>>>(mm, G, cur, scratch, groups, 0, 0, f);
+    kern<<<(unsigned)grid, threads, C::SMEM, s>>>(mm, G, cur, scratch, groups, 0, 0, f);
     *err = cudaGetLastError();
   } else {
     *err = cudaErrorInvalidValue;
@@ -1715,7 +1732,16 @@ cudaError_t launch_fused_step(const MeshDev& m, const double* G, const double* c
   const size_t ring = (size_t)f.rp * m.Mx * m.My;
   static const int dbg = env_int("SFMG_FUSED_DBG", 0);
   f.mode |= dbg;
-  unsigned int* cnt = reinterpret_cast<unsigned int*>((f.mode & 256) ? scratch + m.N - 1024 : scratch + ring);
+  static const int persist_mb = env_int("SFMG_L2_PERSIST_MB", 0);   // developer experiment
+  if (persist_mb > 0) {
+    static bool done = false;
+    if (!done) {
+      cudaError_t pe = cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)persist_mb << 20);
+      fprintf(stderr, "persisting L2 limit %d MB: %s\n", persist_mb, cudaGetErrorString(pe));
+      done = true;
+    }
+  }
+  unsigned int* cnt = reinterpret_cast<unsigned int*>(scratch + ring);
   f.layer_done = cnt;
   f.upd_done = cnt + m.nez;
   f.err = reinterpret_cast<int*>(cnt + 2 * m.nez);

@@ -166,8 +166,8 @@ static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 
 static cudaError_t op_apply(sfmg_level_s* lv, int bc, const double* u, double* v, cudaStream_t s) {
   cudaError_t e;
-  // vectors beyond L2: one fused kernel, A_D u accumulated in an L2-resident plane ring inside lv->y and
-  // copied out one element layer behind (no v init, no RED traffic to HBM)
+  // opt-in (SFMG_FUSED=1): one fused kernel, A_D u accumulated in an L2-resident plane ring inside lv->y
+  // and copied out one element layer behind (no v init, no RED traffic to HBM)
   if (bc == 0 && v != lv->y && u != lv->y && !lv->prof && fused_available(lv->m) && aligned16(u) && aligned16(v)) {
     if ((e = fused_zero_ring(lv->m, lv->y, s))) return e;
     return launch_fused_step(lv->m, lv->G, u, nullptr, v, nullptr, nullptr, lv->y, 0.0, 0.0, 1, s);

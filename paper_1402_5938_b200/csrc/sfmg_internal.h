@@ -183,7 +183,7 @@ cudaError_t launch_load(const MeshDev& m, int rhs_id, double* f, cudaStream_t s)
 cudaError_t launch_cheb_update(const MeshDev& m, const double* cur, const double* prev, double* out,
                                const double* b, double* y, const double* dinv, double c1, double c2,
                                cudaStream_t s);
-// Fused step for vectors beyond L2 (k_apply_v4<.., FU>, 3 <= p <= 8, bc 0): one persistent kernel forms
+// Fused step (k_apply_v4<.., FU>, 3 <= p <= 8, bc 0; opt-in with SFMG_FUSED=1): one persistent kernel forms
 // y = A_D cur in an L2-resident ring of lattice planes and, one element layer behind, mode 0:
 // out = cur + c1 (cur - prev) + c2 dinv (b - y) (prev unused when c1 == 0); mode 1: out = y.
 // scratch: fused_scratch_doubles(m) doubles, ring part all zero on entry (fused_zero_ring) and on exit.
