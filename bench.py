@@ -494,6 +494,8 @@ def run_extras(args, sfmg, dev, stream, flush, hbm_peak):
                           "cheb_step_hbm_frac": alg["step_bytes"] / tc / 1e9 / hbm_peak}
         del lv, u, v, b, x
         torch.cuda.empty_cache()
+        if int(os.environ.get("WORLD_SIZE", "1")) == 1:
+            out["config4"]["fused_step_opt_in"] = fused_config4()
     # config 5: p-MG 16 -> 1, V(2,2) degree-4 Chebyshev, coarse CG 1e-10, PCG to 1e-8
     d = inputs.CONFIG5
     t0 = time.perf_counter()
@@ -572,6 +574,24 @@ def run_extras(args, sfmg, dev, stream, flush, hbm_peak):
         "p%d_%s" % (p, name): timed_solve(dict(nex=32, ney=32, nez=1, p=p, dim=2, quadrature=1), mk("cheb", 2), 1)
         for p in (4, 16) for name, mk in (("pmg", sfmg.MgParams.paper), ("hmg", sfmg.MgParams.paper_h))}
     return out
+
+
+def fused_config4():
+    """The opt-in fused Chebyshev step / apply (one persistent kernel per step, y in an L2-resident plane
+    ring) on config 4, timed by tools/quick_bench.py in a subprocess: the library reads
+    SFMG_FUSED once per process."""
+    import subprocess
+    env = dict(os.environ, SFMG_FUSED="1", SFMG_L2_PERSIST_MB="64")
+    try:
+        r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "quick_bench.py"), "4"], env=env,
+                           capture_output=True, text=True, timeout=600)
+        line = [ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1]
+        d = json.loads(line)
+        return {"apply_ms": d["t_apply_us"] * 1e-3, "apply_hbm_frac": d["frac_hbm_apply"],
+                "cheb_step_ms": d["t_step_us"] * 1e-3, "cheb_step_hbm_frac": d["frac_hbm_step"],
+                "env": "SFMG_FUSED=1 SFMG_L2_PERSIST_MB=64", "timer": "tools/quick_bench.py (CUDA events, L2 flushed)"}
+    except Exception as ex:   # noqa: BLE001  (a measurement key, never the bench's result)
+        return {"error": str(ex)[:200]}
 
 
 def main():

@@ -12,6 +12,7 @@
 // v_e = (B^T x B^T x B^T) v_q; scatter.  G_q = wG_i wG_j wG_k mu(x(xi_q)) detJ_q J_q^{-1} J_q^{-T}
 // with J and x from the isoparametric map evaluated at the Gauss points.
 #include <cmath>
+#include <cstdlib>
 
 #include "k_common.cuh"
 
@@ -30,6 +31,17 @@ constexpr int qvOffset(int P) {
 __constant__ double c_qB[qOffset(kMaxOrder + 1)];
 __constant__ double c_qDB[qOffset(kMaxOrder + 1)];
 __constant__ double c_qDG[qOffset(kMaxOrder + 1)];
+// Even-odd forms of B, DB, B^T, DB^T for even orders 4..8 (k_apply_gauss_v2): B is centro-symmetric
+// (B[n-1-i][n-1-a] = B[i][a]), DB centro-antisymmetric, so a line product splits into an even and an
+// odd half of c = p/2 terms each.  Per set: Me[c][c], Mo[c][c], M[i][c] (c), M[c][m] (c), M[c][c].
+constexpr int geoSize(int P) { return 2 * (P / 2) * (P / 2) + 2 * (P / 2) + 1; }
+constexpr int geoOffset(int P) {
+  int s = 0;
+  for (int q = 4; q < P; q += 2) s += 4 * geoSize(q);
+  return s;
+}
+constexpr int kGaussV2MaxP = 8;
+__constant__ double c_gEO[geoOffset(kGaussV2MaxP + 2)];
 __constant__ double c_qw[qvOffset(kMaxOrder + 1)];   // Gauss weights
 __constant__ double c_qxn[qvOffset(kMaxOrder + 1)];  // LGL nodes (node positions)
 
@@ -139,6 +151,30 @@ cudaError_t upload_gauss_tables(int p) {
   if ((e = cudaMemcpyToSymbol(c_qB, B.data(), sizeof(double) * n * n, mo))) return e;
   if ((e = cudaMemcpyToSymbol(c_qDB, DB.data(), sizeof(double) * n * n, mo))) return e;
   if ((e = cudaMemcpyToSymbol(c_qDG, DG.data(), sizeof(double) * n * n, mo))) return e;
+  if (p % 2 == 0 && p >= 4 && p <= kGaussV2MaxP) {
+    const int c = p / 2;
+    std::vector<double> tab(4 * geoSize(p));
+    for (int set = 0; set < 4; ++set) {
+      auto M = [&](int i, int m2) {
+        switch (set) {
+          case 0: return B[i * n + m2];
+          case 1: return DB[i * n + m2];
+          case 2: return B[m2 * n + i];
+          default: return DB[m2 * n + i];
+        }
+      };
+      double* t = tab.data() + set * geoSize(p);
+      for (int i = 0; i < c; ++i)
+        for (int m2 = 0; m2 < c; ++m2) {
+          t[i * c + m2] = 0.5 * (M(i, m2) + M(i, n - 1 - m2));
+          t[c * c + i * c + m2] = 0.5 * (M(i, m2) - M(i, n - 1 - m2));
+        }
+      for (int i = 0; i < c; ++i) t[2 * c * c + i] = M(i, c);
+      for (int m2 = 0; m2 < c; ++m2) t[2 * c * c + c + m2] = M(c, m2);
+      t[2 * c * c + 2 * c] = M(c, c);
+    }
+    if ((e = cudaMemcpyToSymbol(c_gEO, tab.data(), sizeof(double) * tab.size(), sizeof(double) * geoOffset(p)))) return e;
+  }
   if ((e = cudaMemcpyToSymbol(c_qw, gw.data(), sizeof(double) * n, vo))) return e;
   if ((e = cudaMemcpyToSymbol(c_qxn, L.x.data(), sizeof(double) * n, vo))) return e;
   return cudaSuccess;
@@ -456,6 +492,241 @@ __global__ void __launch_bounds__(GaussCfg<P>::THREADS) k_apply_gauss(MeshDev m,
   }
 }
 
+// ---------------------------------------------------------------------------- apply, v2 (3 <= p <= 8)
+//
+// The gradient at the Gauss points taken directly from the nodal values with DB = D_G B (ell_a'(xi_i)):
+//   g0 = (DB x B x B) u, g1 = (B x DB x B) u, g2 = (B x B x DB) u,   v = the transposed chain of w = G g,
+// sum-factorised as  x: Xb = B u, Xd = DB u;  y: Yb = B Xb, Yd = DB Xb, Y0 = B Xd;
+// z (registers): g0 = B Y0, g1 = B Yd, g2 = DB Yb, w = G g, Z0 = B^T w0, Z1 = B^T w1, Z2 = DB^T w2;
+// y^T: T0 = B^T Z0, Tb = DB^T Z1 + B^T Z2;  x^T: v = DB^T T0 + B^T Tb, RED.
+// 16 line products instead of 12, but 5 block barriers per group instead of 11, three work arrays, every
+// line read once per pass for all its products, and the even-odd split (even p) halves the FMAs.  The
+// factors are staged like the collocated kernel's: one TMA bulk copy per group into shared memory,
+// issued for group g+1 as soon as the z pass of group g has consumed the buffer, plus an L2 prefetch of
+// group g+2 and of the next group's u columns; persistent blocks (grid = occupancy x SMs).
+
+// out = M L on one line: SET 0 B, 1 DB, 2 B^T, 3 DB^T
+template <int P, int SET>
+__device__ __forceinline__ void gline(const double (&L)[P + 1], double (&out)[P + 1]) {
+  constexpr int N = P + 1;
+  if constexpr (P % 2 == 0 && P >= 4) {
+    constexpr int c = P / 2, base = geoOffset(P) + SET * geoSize(P);
+    constexpr bool sym = (SET == 0 || SET == 2);
+    double ev[c], od[c];
+#pragma unroll
+    for (int m = 0; m < c; ++m) {
+      ev[m] = L[m] + L[N - 1 - m];
+      od[m] = L[m] - L[N - 1 - m];
+    }
+#pragma unroll
+    for (int i = 0; i < c; ++i) {
+      double T = c_gEO[base + 2 * c * c + i] * L[c], S = 0.0;
+#pragma unroll
+      for (int m = 0; m < c; ++m) {
+        T = fma(c_gEO[base + i * c + m], ev[m], T);
+        S = fma(c_gEO[base + c * c + i * c + m], od[m], S);
+      }
+      out[i] = T + S;
+      out[N - 1 - i] = sym ? T - S : S - T;
+    }
+    double M = sym ? c_gEO[base + 2 * c * c + 2 * c] * L[c] : 0.0;
+#pragma unroll
+    for (int m = 0; m < c; ++m) M = fma(c_gEO[base + 2 * c * c + c + m], sym ? ev[m] : od[m], M);
+    out[c] = M;
+  } else {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      double s = 0.0;
+#pragma unroll
+      for (int m = 0; m < N; ++m) {
+        const double coef = SET == 0 ? c_qB[qOffset(P) + i * N + m]
+                          : SET == 1 ? c_qDB[qOffset(P) + i * N + m]
+                          : SET == 2 ? c_qB[qOffset(P) + m * N + i]
+                                     : c_qDB[qOffset(P) + m * N + i];
+        s = fma(coef, L[m], s);
+      }
+      out[i] = s;
+    }
+  }
+}
+
+template <int P>
+struct GaussV2Cfg {
+  static constexpr int N = P + 1, N2 = N * N, N3 = N2 * N;
+  static constexpr int PER_ELEM = 9 * N3 * 8;   // 6 n^3 staged factors + three work arrays
+  static constexpr int EPB_SMEM = 53000 / PER_ELEM > 0 ? 53000 / PER_ELEM : 1;
+  static constexpr int EPB_THR = 256 / N2 > 0 ? 256 / N2 : 1;
+  static constexpr int EPB = EPB_SMEM < EPB_THR ? EPB_SMEM : EPB_THR;
+  static constexpr int THREADS = EPB * N2;
+  static constexpr size_t SMEM = (size_t)EPB * PER_ELEM + 16;
+  static constexpr int MINB = (227 * 1024) / (SMEM + 1024) < 8 ? (227 * 1024) / (SMEM + 1024) : 8;
+};
+
+template <int P, bool DIR>
+__global__ void __launch_bounds__(GaussV2Cfg<P>::THREADS, GaussV2Cfg<P>::MINB)
+    k_apply_gauss_v2(MeshDev m, const double* __restrict__ G, const double* __restrict__ u, double* __restrict__ v) {
+  using C = GaussV2Cfg<P>;
+  constexpr int N = C::N, N2 = C::N2, N3 = C::N3;
+  extern __shared__ __align__(128) double gsm2[];
+  double* sG = gsm2;                                   // [EPB][k][6][n^2]
+  const int le = threadIdx.x / N2, t = threadIdx.x - le * N2, t0 = t % N, t1 = t / N;
+  double* A0 = gsm2 + C::EPB * 6 * N3 + le * 3 * N3;
+  double* A1 = A0 + N3;
+  double* A2 = A1 + N3;
+  uint64_t* bar = (uint64_t*)(gsm2 + C::EPB * 9 * N3);
+  const double* gE = sG + le * 6 * N3;
+  const long long sxy = (long long)m.Mx * m.My;
+  const long long ngroups = (m.E + C::EPB - 1) / C::EPB;
+  const long long gstride = gridDim.x;
+  auto group_bytes = [&](long long g) -> unsigned {
+    long long nel = m.E - g * C::EPB;
+    if (nel > C::EPB) nel = C::EPB;
+    return (unsigned)(nel * 6 * N3 * sizeof(double));
+  };
+  auto prefetch_columns = [&](long long g) {
+    const long long en = g * C::EPB + le;
+    if (en >= m.E) return;
+    int qx, qy, qz;
+    elem_coords(m, en, qx, qy, qz);
+    const double* pu = u + (long long)(qx * P + t0) + (long long)m.Mx * (qy * P + t1) + sxy * (long long)(qz * P);
+#pragma unroll
+    for (int c = 0; c < N; ++c) asm volatile("prefetch.global.L2 [%0];" ::"l"(pu + sxy * c));
+  };
+  long long grp = blockIdx.x;
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    if (grp < ngroups) bulk_load(sG, G + grp * C::EPB * 6 * N3, group_bytes(grp), bar);
+    if (grp + gstride < ngroups) gauss_prefetch_l2(G + (grp + gstride) * C::EPB * 6 * N3, group_bytes(grp + gstride));
+  }
+  unsigned phase = 0;
+  for (; grp < ngroups; grp += gstride) {
+    const long long e = grp * C::EPB + le;
+    const bool act = e < m.E;
+    int ex = 0, ey = 0, ez = 0;
+    if (act) elem_coords(m, e, ex, ey, ez);
+    if (grp + gstride < ngroups) prefetch_columns(grp + gstride);
+    {  // gather: nodal column (a = t0, b = t1), masked (R4)
+      const int I = ex * P + t0, J = ey * P + t1;
+      const long long col = (long long)I + (long long)m.Mx * J + sxy * (long long)(ez * P);
+#pragma unroll
+      for (int c = 0; c < N; ++c) {
+        const int K = ez * P + c;
+        const bool bnd = DIR && (I == 0 || I == m.Mx - 1 || J == 0 || J == m.My - 1 || K == m.Kb0 || K == m.Kb1);
+        A0[t + N2 * c] = (act && !bnd) ? __ldg(u + col + sxy * c) : 0.0;
+      }
+    }
+    __syncthreads();
+    {  // x: line (b = t0, c = t1): Xb = B u -> A1, Xd = DB u -> A2
+      double L[N], o[N];
+#pragma unroll
+      for (int a = 0; a < N; ++a) L[a] = A0[a + N * t0 + N2 * t1];
+      gline<P, 0>(L, o);
+#pragma unroll
+      for (int i = 0; i < N; ++i) A1[i + N * t0 + N2 * t1] = o[i];
+      gline<P, 1>(L, o);
+#pragma unroll
+      for (int i = 0; i < N; ++i) A2[i + N * t0 + N2 * t1] = o[i];
+    }
+    __syncthreads();
+    {  // y: line (i = t0, c = t1): Yb = B Xb -> A0, Yd = DB Xb -> A1 (in place), Y0 = B Xd -> A2 (in place)
+      double L[N], o[N];
+      const int yb = t0 + N2 * t1;
+#pragma unroll
+      for (int b = 0; b < N; ++b) L[b] = A1[yb + N * b];
+      gline<P, 0>(L, o);
+#pragma unroll
+      for (int j = 0; j < N; ++j) A0[yb + N * j] = o[j];
+      gline<P, 1>(L, o);
+#pragma unroll
+      for (int j = 0; j < N; ++j) A1[yb + N * j] = o[j];
+#pragma unroll
+      for (int b = 0; b < N; ++b) L[b] = A2[yb + N * b];
+      gline<P, 0>(L, o);
+#pragma unroll
+      for (int j = 0; j < N; ++j) A2[yb + N * j] = o[j];
+    }
+    __syncthreads();
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    {  // z in registers: column (i = t0, j = t1)
+      double L[N], g0[N], g1[N], g2[N];
+#pragma unroll
+      for (int c = 0; c < N; ++c) L[c] = A2[t + N2 * c];
+      gline<P, 0>(L, g0);
+#pragma unroll
+      for (int c = 0; c < N; ++c) L[c] = A1[t + N2 * c];
+      gline<P, 0>(L, g1);
+#pragma unroll
+      for (int c = 0; c < N; ++c) L[c] = A0[t + N2 * c];
+      gline<P, 1>(L, g2);
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        const double* Gk = gE + gofs<N>(0, t, k);
+        const double G00 = Gk[0], G01 = Gk[N2], G02 = Gk[2 * N2], G11 = Gk[3 * N2], G12 = Gk[4 * N2], G22 = Gk[5 * N2];
+        const double a0 = g0[k], a1 = g1[k], a2 = g2[k];
+        g0[k] = G00 * a0 + G01 * a1 + G02 * a2;
+        g1[k] = G01 * a0 + G11 * a1 + G12 * a2;
+        g2[k] = G02 * a0 + G12 * a1 + G22 * a2;
+      }
+      gline<P, 2>(g0, L);
+#pragma unroll
+      for (int c = 0; c < N; ++c) A2[t + N2 * c] = L[c];
+      gline<P, 2>(g1, L);
+#pragma unroll
+      for (int c = 0; c < N; ++c) A1[t + N2 * c] = L[c];
+      gline<P, 3>(g2, L);
+#pragma unroll
+      for (int c = 0; c < N; ++c) A0[t + N2 * c] = L[c];
+    }
+    __syncthreads();
+    {  // factors consumed: next group's TMA copy and the L2 prefetch of the group after
+      const long long nx = grp + gstride;
+      if (nx < ngroups && threadIdx.x == 0) {
+        fence_proxy_async_smem();
+        bulk_load(sG, G + nx * C::EPB * 6 * N3, group_bytes(nx), bar);
+        if (nx + gstride < ngroups) gauss_prefetch_l2(G + (nx + gstride) * C::EPB * 6 * N3, group_bytes(nx + gstride));
+      }
+    }
+    {  // y^T: line (i = t0, c = t1): T0 = B^T Z0 -> A2 (in place), Tb = DB^T Z1 + B^T Z2 -> A1 (in place)
+      double L[N], o[N], o2[N];
+      const int yb = t0 + N2 * t1;
+#pragma unroll
+      for (int j = 0; j < N; ++j) L[j] = A2[yb + N * j];
+      gline<P, 2>(L, o);
+#pragma unroll
+      for (int b = 0; b < N; ++b) A2[yb + N * b] = o[b];
+#pragma unroll
+      for (int j = 0; j < N; ++j) L[j] = A1[yb + N * j];
+      gline<P, 3>(L, o);
+#pragma unroll
+      for (int j = 0; j < N; ++j) L[j] = A0[yb + N * j];
+      gline<P, 2>(L, o2);
+#pragma unroll
+      for (int b = 0; b < N; ++b) A1[yb + N * b] = o[b] + o2[b];
+    }
+    __syncthreads();
+    if (act) {  // x^T: line (b = t0, c = t1): v = DB^T T0 + B^T Tb, scatter (fp64 RED)
+      double L[N], o[N], o2[N];
+#pragma unroll
+      for (int i = 0; i < N; ++i) L[i] = A2[i + N * t0 + N2 * t1];
+      gline<P, 3>(L, o);
+#pragma unroll
+      for (int i = 0; i < N; ++i) L[i] = A1[i + N * t0 + N2 * t1];
+      gline<P, 2>(L, o2);
+      const int J = ey * P + t0, K = ez * P + t1;
+      const long long row = (long long)m.Mx * J + sxy * K + (long long)ex * P;
+#pragma unroll
+      for (int a = 0; a < N; ++a) {
+        const int I = ex * P + a;
+        const bool bnd = DIR && (I == 0 || I == m.Mx - 1 || J == 0 || J == m.My - 1 || K == m.Kb0 || K == m.Kb1);
+        if (!bnd) atomicAdd(v + row + a, o[a] + o2[a]);
+      }
+    }
+    // (the next gather writes A0, last read before the barrier above; A1 / A2 are rewritten only after
+    //  the barrier that follows the gather)
+  }
+}
+
 // ---------------------------------------------------------------------------- diagonal
 
 // d_l = sum_q grad phi_l(q)^T G_q grad phi_l(q), grad phi_l(q) = (DB_ia B_jb B_kc, B_ia DB_jb B_kc,
@@ -769,8 +1040,40 @@ cudaError_t launch_geometry_gauss(const MeshDev& m, double* G, int* bad, cudaStr
   SFMG_GAUSS_DISPATCH(m.p, geometry_g, m, G, bad, s);
 }
 
+// SFMG_GAUSS_V1=1: the round-1 kernel for every order (A/B measurements)
+static bool gauss_v1_forced() {
+  static const bool on = [] {
+    const char* e = getenv("SFMG_GAUSS_V1");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
+template <int P, bool DIR>
+static cudaError_t apply_g_v2(const MeshDev& m, const double* G, const double* u, double* v, cudaStream_t s) {
+  using C = GaussV2Cfg<P>;
+  static IntPerDevice occ;
+  int per_sm = 0;
+  cudaError_t e = occ.get(per_sm, [&](int& n) {
+    cudaError_t r = cudaFuncSetAttribute(k_apply_gauss_v2<P, DIR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)C::SMEM);
+    if (r) return r;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_apply_gauss_v2<P, DIR>, C::THREADS, C::SMEM);
+  });
+  if (e) return e;
+  const long long groups = (m.E + C::EPB - 1) / C::EPB;
+  long long grid = (long long)per_sm * num_sms();
+  if (grid > groups) grid = groups;
+  k_apply_gauss_v2<P, DIR><<<(unsigned)grid, C::THREADS, C::SMEM, s>>>(m, G, u, v);
+  return cudaGetLastError();
+}
+
 template <int P>
 static cudaError_t apply_g(const MeshDev& m, int bc, const double* G, const double* u, double* v, cudaStream_t s) {
+  if constexpr (P >= 3 && P <= kGaussV2MaxP) {
+    if (!gauss_v1_forced())
+      return bc == 0 ? apply_g_v2<P, true>(m, G, u, v, s) : apply_g_v2<P, false>(m, G, u, v, s);
+  }
   using C = GaussCfg<P>;
   static OncePerDevice attr;
   {

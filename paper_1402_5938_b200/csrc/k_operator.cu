@@ -214,52 +214,6 @@ __global__ void __launch_bounds__(256) k_geometry(MeshDev m, double* __restrict_
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
-// TMA / mbarrier / cp.async helpers (inline PTX).
-
-__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-
-// The geometric factors are the one stream read exactly once per apply (48 B per point, ~80 % of the
-// bytes); their bulk copies and L2 prefetches carry an L2 evict-first policy so that the streamed
-// factors do not push u and the RED target v (each touched by up to 8 elements, at different times)
-// out of L2.
-__device__ __forceinline__ uint64_t l2_evict_first_policy() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(l2_evict_first_policy())
-      : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
-  asm volatile(
-      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
-          smem_u32(bar)),
-      "r"(phase)
-      : "memory");
-}
-
-__device__ __forceinline__ void bulk_prefetch_l2(const void* src, unsigned bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(src), "r"(bytes),
-               "l"(l2_evict_first_policy())
-               : "memory");
-}
-
-__device__ __forceinline__ void fence_proxy_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-
-
 // ------------------------------------------------------------------------------------------
 // K2 apply, v4 (p >= 3): persistent, software-pipelined across element groups.
 // Block = EPB elements x (n x n) threads; thread t = (t0, t1) of an element owns one 1-D line per
@@ -365,6 +319,7 @@ struct FusedArgs {
   int mode = 0;    // 0 Chebyshev / Jacobi update, 1 out = A_D x (ring copied out, boundary rows = x)
   long long gpl = 0, shift = 0;
   unsigned chunk = 0, chunk_last = 0;   // nodes per update piece (even), inner plane sets / the last one
+  int color = 0;                        // COL: element colour of this launch
 };
 
 // Explicit reductions: in the fused kernel ptxas keeps atomicAdd as the value-returning ATOMG (the
@@ -529,7 +484,11 @@ __device__ __forceinline__ void fused_piece(const MeshDev& m, const double* cur,
 // zero there beforehand, as the init kernels leave it).  Used for vectors larger than L2 (N > 2^24)
 // right after the v init, where a RED into a line that the init already evicted costs an HBM read; for
 // L2-resident vectors the REDs are cheaper (config 2 measured slower with plain stores).
-template <int P, bool DIR, bool GS, bool IPS = false, bool FU = false>
+// COL (measurement variant, SFMG_COLOR=1; EPB = 1 orders only): one launch per element colour
+// (ex & 1, ey & 1, ez & 1) -- elements of one colour share no node, so the scatter is a plain
+// load-add-store instead of an fp64 RED (north_star: "element coloring or atomics, whichever ncu favours";
+// measured in profiles/r02_experiments.md).
+template <int P, bool DIR, bool GS, bool IPS = false, bool FU = false, bool COL = false>
 __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
     k_apply_v4(MeshDev m, const double* __restrict__ G, const double* __restrict__ u, double* __restrict__ v,
                long long ngroups, int wait_mode, int write_bnd, FusedArgs f) {
@@ -558,19 +517,32 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
   const double* gE = sG + le * 6 * N3;
   const long long sxy = (long long)m.Mx * m.My;
   const long long gstride = gridDim.x;
+  if constexpr (COL) static_assert(C::EPB == 1 && !FU && !IPS, "coloured variant: one element per block");
+  // first element of group g (COL: the g-th element of colour f.color, x fastest)
+  auto gfirst = [&](long long g) -> long long {
+    if constexpr (COL) {
+      const int cx = f.color & 1, cy = (f.color >> 1) & 1, cz = (f.color >> 2) & 1;
+      const unsigned nxc = (unsigned)(m.nex - cx + 1) >> 1, nyc = (unsigned)(m.ney - cy + 1) >> 1;
+      const unsigned ug = (unsigned)g, tq = ug / nxc, ix = ug - tq * nxc, iz = tq / nyc, iy = tq - iz * nyc;
+      (void)cz;
+      return (long long)(2 * ix + cx) + (long long)m.nex * ((2 * iy + cy) + (long long)m.ney * (2 * iz + cz));
+    } else {
+      return g * C::EPB;
+    }
+  };
   auto group_bytes = [&](long long g) -> unsigned {
-    long long nel = m.E - g * C::EPB;
+    long long nel = m.E - gfirst(g);
     if (nel > C::EPB) nel = C::EPB;
     return (unsigned)(nel * 6 * N3 * sizeof(double));
   };
   auto prefetch_group_l2 = [&](long long g) {   // TMA L2 prefetch in <= 64 KB pieces
-    const char* src = (const char*)(G + g * C::EPB * 6 * N3);
+    const char* src = (const char*)(G + gfirst(g) * 6 * N3);
     const unsigned total = group_bytes(g);
     for (unsigned o = 0; o < total; o += 65536u) bulk_prefetch_l2(src + o, total - o < 65536u ? total - o : 65536u);
   };
   // this thread's u column of group g (M u: zero outside the element / on Dirichlet nodes, R4)
   auto load_column = [&](long long g, double (&r)[N]) {
-    const long long e = g * C::EPB + le;
+    const long long e = gfirst(g) + le;
     const bool act = e < m.E;
     int ex = 0, ey = 0, ez = 0;
     if (act) elem_coords(m, e, ex, ey, ez);
@@ -588,7 +560,7 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
     }
   };
   auto prefetch_column = [&](long long g) {
-    const long long e = g * C::EPB + le;
+    const long long e = gfirst(g) + le;
     if (e >= m.E) return;
     int ex, ey, ez;
     elem_coords(m, e, ex, ey, ez);
@@ -607,7 +579,7 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
   if (threadIdx.x == 0) {   // factor prefetches need nothing from the predecessor kernel
     if (GS) {
       mbar_init(bar, 1);
-      if (grp < ngroups) bulk_load(sG, G + grp * C::EPB * 6 * N3, group_bytes(grp), bar);
+      if (grp < ngroups) bulk_load(sG, G + gfirst(grp) * 6 * N3, group_bytes(grp), bar);
     } else if (grp < ngroups) {
       prefetch_group_l2(grp);
     }
@@ -640,7 +612,7 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
     // waits (griddepcontrol.wait) for this grid's completion before reading v.  Small vectors only
     // (config 4 measured 2.51 -> 2.61 ms with it)
     if (m.pdl_early && grp + gstride >= ngroups) pdl_trigger();
-    const long long e = grp * C::EPB + le;
+    const long long e = gfirst(grp) + le;
     const bool act = e < m.E;
     int ex = 0, ey = 0, ez = 0;
     if (act) elem_coords(m, e, ex, ey, ez);
@@ -776,7 +748,7 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
       if (nx < ngroups && threadIdx.x == 0) {
         if (GS) {
           fence_proxy_async_smem();
-          bulk_load(sG, G + nx * C::EPB * 6 * N3, group_bytes(nx), bar);
+          bulk_load(sG, G + gfirst(nx) * 6 * N3, group_bytes(nx), bar);
         }
         if (PF == 2 && nx + gstride < ngroups) prefetch_group_l2(nx + gstride);
         else if (!GS && nx < ngroups) prefetch_group_l2(nx);
@@ -872,6 +844,7 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
           if (!bnd) ring_red(v + gxy + sxy * slot, xy + vz[c], rpol);
           else if (own_xy && (c > 0 || ez == 0)) ring_st(v + gxy + sxy * slot, u[gcol + sxy * c], rpol);   // A_D x = x (R4)
         } else if (IPS && t0 > 0 && t0 < P && t1 > 0 && t1 < P && c > 0 && c < P) v[gcol + sxy * c] = xy + vz[c];
+        else if (COL) { if (!bnd) v[gcol + sxy * c] += xy + vz[c]; }
         else if (!bnd) atomicAdd(v + gcol + sxy * c, xy + vz[c]);
         else if (write_bnd && own_xy && (c > 0 || ez == 0)) v[gcol + sxy * c] = u[gcol + sxy * c];  // (I-M) u
       }
@@ -1533,6 +1506,14 @@ static bool ks_enabled() {
   return on;
 }
 
+static bool color_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("SFMG_COLOR");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 template <int P, bool DIR, bool IPS>
 static cudaError_t launch_ks(const MeshDev& m, const double* G, const double* u, double* v, int wait_mode,
                              int write_bnd, cudaStream_t s) {
@@ -1592,7 +1573,32 @@ static cudaError_t apply_pd(const MeshDev& m, const double* G, const double* u, 
     using C = V4Cfg<P, GS>;
     static IntPerDevice occ, occ_ips;
     int resident = 0;
-    cudaError_t e = persistent_blocks(occ, k_apply_v4<P, DIR, GS>, C::THREADS, C::SMEM, resident);
+    cudaError_t e;
+    if constexpr (GS && C::EPB == 1) {
+      if (color_enabled()) {   // measurement variant: eight coloured launches with plain load-add-stores
+        static IntPerDevice occ_col;
+        auto kc = k_apply_v4<P, DIR, GS, false, false, true>;
+        if ((e = persistent_blocks(occ_col, kc, C::THREADS, C::SMEM, resident))) return e;
+        MeshDev mm = m;
+        mm.pdl_early = 0;
+        for (int c = 0; c < 8; ++c) {
+          const long long nc = (long long)((m.nex - (c & 1) + 1) / 2) * ((m.ney - ((c >> 1) & 1) + 1) / 2) *
+                               ((m.nez - ((c >> 2) & 1) + 1) / 2);
+          if (nc == 0) continue;
+          long long grid = (long long)resident * num_sms();
+          if (grid > nc) grid = nc;
+          FusedArgs fa;
+          fa.color = c;
+          // (programmatic launch: a coloured launch starts its factor prefetch during the previous one's
+          // tail and waits for its completion before the gather)
+          if ((e = launch_pdl(kc, (unsigned)grid, (unsigned)C::THREADS, C::SMEM, s, mm, G, u, v, nc,
+                              c == 0 ? wait_mode : 2, write_bnd, fa)))
+            return e;
+        }
+        return cudaSuccess;
+      }
+    }
+    e = persistent_blocks(occ, k_apply_v4<P, DIR, GS>, C::THREADS, C::SMEM, resident);
     if (e) return e;
     const long long groups = (m.E + C::EPB - 1) / C::EPB;
     long long grid = (long long)resident * num_sms();

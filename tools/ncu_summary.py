@@ -15,12 +15,18 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
 STALLS = "smsp__average_warps_issue_stalled_"
 
 
-def main(path):
+def main(path, unique=False):
     out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
     hdr, units = rows[0], rows[1]
+    seen = set()
     for r in rows[2:]:
         d = dict(zip(hdr, r))
+        if unique:   # one launch per (kernel, grid, block): the first
+            key = (d.get("Kernel Name", ""), d.get("launch__grid_size", ""), d.get("launch__block_size", ""))
+            if key in seen:
+                continue
+            seen.add(key)
         u = dict(zip(hdr, units))
         print("==", d.get("Kernel Name", "")[:100])
         for k in KEYS:
@@ -34,4 +40,4 @@ def main(path):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1])
+    main(sys.argv[1], len(sys.argv) > 2 and sys.argv[2] == "--unique")
