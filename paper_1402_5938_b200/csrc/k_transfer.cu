@@ -44,7 +44,7 @@ struct XferCfg {
   static constexpr int T1 = NF * NC * NC, T2 = NF * NF * NC;      // prolong intermediates
   static constexpr int R1 = NC * NF * NF, R2 = NC * NC * NF;      // restrict intermediates
   static constexpr size_t SMEM_P = sizeof(double) * (NC3 + T1 + T2 + NF * NC);   // + I (k_prolong)
-  static constexpr size_t SMEM_R = sizeof(double) * (NF3 + R1 + R2);
+  static constexpr size_t SMEM_R = sizeof(double) * NF3;   // the three passes run in place
 };
 
 // Prolongation: thread per output value in each pass, I copied to shared memory (a thread-dependent
@@ -105,7 +105,10 @@ __global__ void __launch_bounds__(256) k_prolong(MeshDev mc, MeshDev mf, const d
     double s = 0.0;
 #pragma unroll
     for (int c = 0; c < NC; ++c) s += I[k * NC + c] * t2[i + NF * (j + NF * c)];
-    if (add) uf[g] += s; else uf[g] = s;
+    // add: one fp64 RED per node (each fine node has exactly one owner, so the result is the same single
+    // rounding of uf + s as a load-add-store, without the dependent L2 round trip per output:
+    // k_prolong<8> 36 -> see profiles/r02_experiments.md)
+    if (add) atomicAdd(uf + g, s); else uf[g] = s;
   }
 }
 
@@ -115,9 +118,11 @@ __global__ void __launch_bounds__(kXferThreads) k_restrict(MeshDev mc, MeshDev m
   using C = XferCfg<PC>;
   constexpr int NC = C::NC, NF = C::NF, PF = C::PF;
   extern __shared__ double sm[];
-  double* sf = sm;             // [k][j][i]
-  double* t1 = sf + C::NF3;    // [k][j][a]
-  double* t2 = t1 + C::R1;     // [k][b][a]
+  // One array, the passes in place (a line is read and rewritten by one thread): fine values [k][j][i],
+  // after x the coarse a sits in slot i = a, after y the coarse b in slot j = b.  39 KB at pc = 8, so
+  // five blocks per SM and all 512 blocks of the config-5 fine level resident at once (the three-array
+  // form held 71 KB: 3 blocks per SM, two waves).
+  double* sf = sm;
   const double* I = c_I[PC - 1];
   const long long e = blockIdx.x;
   int ex, ey, ez;
@@ -142,7 +147,7 @@ __global__ void __launch_bounds__(kXferThreads) k_restrict(MeshDev mc, MeshDev m
       double acc = 0.0;
 #pragma unroll
       for (int i = 0; i < NF; ++i) acc = fma(I[i * NC + a], L[i], acc);
-      t1[a + NC * r] = acc;
+      sf[a + NF * r] = acc;
     }
   }
   __syncthreads();
@@ -150,13 +155,13 @@ __global__ void __launch_bounds__(kXferThreads) k_restrict(MeshDev mc, MeshDev m
     const int a = r % NC, k = r / NC;
     double L[NF];
 #pragma unroll
-    for (int j = 0; j < NF; ++j) L[j] = t1[a + NC * (j + NF * k)];
+    for (int j = 0; j < NF; ++j) L[j] = sf[a + NF * (j + NF * k)];
 #pragma unroll
     for (int b = 0; b < NC; ++b) {
       double acc = 0.0;
 #pragma unroll
       for (int j = 0; j < NF; ++j) acc = fma(I[j * NC + b], L[j], acc);
-      t2[a + NC * (b + NC * k)] = acc;
+      sf[a + NF * (b + NF * k)] = acc;
     }
   }
   __syncthreads();
@@ -166,7 +171,7 @@ __global__ void __launch_bounds__(kXferThreads) k_restrict(MeshDev mc, MeshDev m
     if (I0 == 0 || I0 == mc.Mx - 1 || J0 == 0 || J0 == mc.My - 1) continue;
     double L[NF];
 #pragma unroll
-    for (int k = 0; k < NF; ++k) L[k] = t2[r + NC * NC * k];
+    for (int k = 0; k < NF; ++k) L[k] = sf[a + NF * (b + NF * k)];
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
       const int K0 = ez * PC + c;
