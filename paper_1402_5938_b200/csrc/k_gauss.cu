@@ -31,7 +31,7 @@ constexpr int qvOffset(int P) {
 __constant__ double c_qB[qOffset(kMaxOrder + 1)];
 __constant__ double c_qDB[qOffset(kMaxOrder + 1)];
 __constant__ double c_qDG[qOffset(kMaxOrder + 1)];
-// Even-odd forms of B, DB, B^T, DB^T for even orders 4..8 (k_apply_gauss_v2): B is centro-symmetric
+// Even-odd forms of B, DB, B^T, DB^T for even orders 4..16 (k_apply_gauss_v2): B is centro-symmetric
 // (B[n-1-i][n-1-a] = B[i][a]), DB centro-antisymmetric, so a line product splits into an even and an
 // odd half of c = p/2 terms each.  Per set: Me[c][c], Mo[c][c], M[i][c] (c), M[c][m] (c), M[c][c].
 constexpr int geoSize(int P) { return 2 * (P / 2) * (P / 2) + 2 * (P / 2) + 1; }
@@ -40,7 +40,7 @@ constexpr int geoOffset(int P) {
   for (int q = 4; q < P; q += 2) s += 4 * geoSize(q);
   return s;
 }
-constexpr int kGaussV2MaxP = 8;
+constexpr int kGaussV2MaxP = 16;
 __constant__ double c_gEO[geoOffset(kGaussV2MaxP + 2)];
 __constant__ double c_qw[qvOffset(kMaxOrder + 1)];   // Gauss weights
 __constant__ double c_qxn[qvOffset(kMaxOrder + 1)];  // LGL nodes (node positions)
@@ -492,7 +492,7 @@ __global__ void __launch_bounds__(GaussCfg<P>::THREADS) k_apply_gauss(MeshDev m,
   }
 }
 
-// ---------------------------------------------------------------------------- apply, v2 (3 <= p <= 8)
+// ---------------------------------------------------------------------------- apply, v2 (3 <= p <= 16)
 //
 // The gradient at the Gauss points taken directly from the nodal values with DB = D_G B (ell_a'(xi_i)):
 //   g0 = (DB x B x B) u, g1 = (B x DB x B) u, g2 = (B x B x DB) u,   v = the transposed chain of w = G g,
@@ -550,16 +550,21 @@ __device__ __forceinline__ void gline(const double (&L)[P + 1], double (&out)[P 
   }
 }
 
+// GS (p <= 8): the group's factors are staged in shared memory by TMA; p >= 9 (an element's factors are up
+// to 236 KB): the pointwise pass reads them from L2 (streaming loads; the group was L2-prefetched).
 template <int P>
 struct GaussV2Cfg {
   static constexpr int N = P + 1, N2 = N * N, N3 = N2 * N;
-  static constexpr int PER_ELEM = 9 * N3 * 8;   // 6 n^3 staged factors + three work arrays
+  static constexpr bool GS = P <= 8;
+  static constexpr int ARR = GS ? 9 : 3;           // n^3 arrays per element: (6 staged factors +) three work arrays
+  static constexpr int PER_ELEM = ARR * N3 * 8;
   static constexpr int EPB_SMEM = 53000 / PER_ELEM > 0 ? 53000 / PER_ELEM : 1;
   static constexpr int EPB_THR = 256 / N2 > 0 ? 256 / N2 : 1;
   static constexpr int EPB = EPB_SMEM < EPB_THR ? EPB_SMEM : EPB_THR;
   static constexpr int THREADS = EPB * N2;
   static constexpr size_t SMEM = (size_t)EPB * PER_ELEM + 16;
-  static constexpr int MINB = (227 * 1024) / (SMEM + 1024) < 8 ? (227 * 1024) / (SMEM + 1024) : 8;
+  static constexpr int MINB_SMEM = (227 * 1024) / (SMEM + 1024) < 8 ? (227 * 1024) / (SMEM + 1024) : 8;
+  static constexpr int MINB = GS ? MINB_SMEM : (P >= 12 ? 1 : 2);   // p >= 9: the register file decides
 };
 
 template <int P, bool DIR>
@@ -567,13 +572,14 @@ __global__ void __launch_bounds__(GaussV2Cfg<P>::THREADS, GaussV2Cfg<P>::MINB)
     k_apply_gauss_v2(MeshDev m, const double* __restrict__ G, const double* __restrict__ u, double* __restrict__ v) {
   using C = GaussV2Cfg<P>;
   constexpr int N = C::N, N2 = C::N2, N3 = C::N3;
+  constexpr bool GS = C::GS;
   extern __shared__ __align__(128) double gsm2[];
-  double* sG = gsm2;                                   // [EPB][k][6][n^2]
+  double* sG = gsm2;                                   // [EPB][k][6][n^2] (GS)
   const int le = threadIdx.x / N2, t = threadIdx.x - le * N2, t0 = t % N, t1 = t / N;
-  double* A0 = gsm2 + C::EPB * 6 * N3 + le * 3 * N3;
+  double* A0 = gsm2 + (GS ? C::EPB * 6 * N3 : 0) + le * 3 * N3;
   double* A1 = A0 + N3;
   double* A2 = A1 + N3;
-  uint64_t* bar = (uint64_t*)(gsm2 + C::EPB * 9 * N3);
+  uint64_t* bar = (uint64_t*)(gsm2 + C::EPB * C::ARR * N3);
   const double* gE = sG + le * 6 * N3;
   const long long sxy = (long long)m.Mx * m.My;
   const long long ngroups = (m.E + C::EPB - 1) / C::EPB;
@@ -594,9 +600,13 @@ __global__ void __launch_bounds__(GaussV2Cfg<P>::THREADS, GaussV2Cfg<P>::MINB)
   };
   long long grp = blockIdx.x;
   if (threadIdx.x == 0) {
-    mbar_init(bar, 1);
-    if (grp < ngroups) bulk_load(sG, G + grp * C::EPB * 6 * N3, group_bytes(grp), bar);
-    if (grp + gstride < ngroups) gauss_prefetch_l2(G + (grp + gstride) * C::EPB * 6 * N3, group_bytes(grp + gstride));
+    if (GS) {
+      mbar_init(bar, 1);
+      if (grp < ngroups) bulk_load(sG, G + grp * C::EPB * 6 * N3, group_bytes(grp), bar);
+      if (grp + gstride < ngroups) gauss_prefetch_l2(G + (grp + gstride) * C::EPB * 6 * N3, group_bytes(grp + gstride));
+    } else if (grp < ngroups) {
+      gauss_prefetch_l2(G + grp * C::EPB * 6 * N3, group_bytes(grp));
+    }
   }
   unsigned phase = 0;
   for (; grp < ngroups; grp += gstride) {
@@ -646,9 +656,11 @@ __global__ void __launch_bounds__(GaussV2Cfg<P>::THREADS, GaussV2Cfg<P>::MINB)
       for (int j = 0; j < N; ++j) A2[yb + N * j] = o[j];
     }
     __syncthreads();
-    mbar_wait(bar, phase);
-    phase ^= 1u;
-    {  // z in registers: column (i = t0, j = t1)
+    if (GS) {
+      mbar_wait(bar, phase);
+      phase ^= 1u;
+    }
+    if constexpr (GS) {  // z in registers: column (i = t0, j = t1)
       double L[N], g0[N], g1[N], g2[N];
 #pragma unroll
       for (int c = 0; c < N; ++c) L[c] = A2[t + N2 * c];
@@ -661,8 +673,15 @@ __global__ void __launch_bounds__(GaussV2Cfg<P>::THREADS, GaussV2Cfg<P>::MINB)
       gline<P, 1>(L, g2);
 #pragma unroll
       for (int k = 0; k < N; ++k) {
-        const double* Gk = gE + gofs<N>(0, t, k);
-        const double G00 = Gk[0], G01 = Gk[N2], G02 = Gk[2 * N2], G11 = Gk[3 * N2], G12 = Gk[4 * N2], G22 = Gk[5 * N2];
+        double G00, G01, G02, G11, G12, G22;
+        if (GS) {
+          const double* Gk = gE + gofs<N>(0, t, k);
+          G00 = Gk[0]; G01 = Gk[N2]; G02 = Gk[2 * N2]; G11 = Gk[3 * N2]; G12 = Gk[4 * N2]; G22 = Gk[5 * N2];
+        } else {
+          const double* Gk = G + (act ? e : 0) * 6 * N3 + gofs<N>(0, t, k);
+          G00 = __ldcs(Gk); G01 = __ldcs(Gk + N2); G02 = __ldcs(Gk + 2 * N2);
+          G11 = __ldcs(Gk + 3 * N2); G12 = __ldcs(Gk + 4 * N2); G22 = __ldcs(Gk + 5 * N2);
+        }
         const double a0 = g0[k], a1 = g1[k], a2 = g2[k];
         g0[k] = G00 * a0 + G01 * a1 + G02 * a2;
         g1[k] = G01 * a0 + G11 * a1 + G12 * a2;
@@ -677,14 +696,58 @@ __global__ void __launch_bounds__(GaussV2Cfg<P>::THREADS, GaussV2Cfg<P>::MINB)
       gline<P, 3>(g2, L);
 #pragma unroll
       for (int c = 0; c < N; ++c) A0[t + N2 * c] = L[c];
+    } else {  // p >= 9: the same z pass one line product at a time through the thread's own columns of
+              // A0 / A1 / A2 (three 17-value register arrays at once would spill)
+      double L[N], o[N];
+#pragma unroll
+      for (int c = 0; c < N; ++c) L[c] = A2[t + N2 * c];
+      gline<P, 0>(L, o);
+#pragma unroll
+      for (int k = 0; k < N; ++k) A2[t + N2 * k] = o[k];
+#pragma unroll
+      for (int c = 0; c < N; ++c) L[c] = A1[t + N2 * c];
+      gline<P, 0>(L, o);
+#pragma unroll
+      for (int k = 0; k < N; ++k) A1[t + N2 * k] = o[k];
+#pragma unroll
+      for (int c = 0; c < N; ++c) L[c] = A0[t + N2 * c];
+      gline<P, 1>(L, o);   // g2 stays in registers (o)
+      const double* Ge = G + (act ? e : 0) * 6 * N3;
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        const double* Gk = Ge + gofs<N>(0, t, k);
+        const double G00 = __ldcs(Gk), G01 = __ldcs(Gk + N2), G02 = __ldcs(Gk + 2 * N2);
+        const double G11 = __ldcs(Gk + 3 * N2), G12 = __ldcs(Gk + 4 * N2), G22 = __ldcs(Gk + 5 * N2);
+        const double a0 = A2[t + N2 * k], a1 = A1[t + N2 * k], a2 = o[k];
+        A2[t + N2 * k] = G00 * a0 + G01 * a1 + G02 * a2;
+        A1[t + N2 * k] = G01 * a0 + G11 * a1 + G12 * a2;
+        o[k] = G02 * a0 + G12 * a1 + G22 * a2;
+      }
+      gline<P, 3>(o, L);
+#pragma unroll
+      for (int c = 0; c < N; ++c) A0[t + N2 * c] = L[c];
+#pragma unroll
+      for (int k = 0; k < N; ++k) L[k] = A2[t + N2 * k];
+      gline<P, 2>(L, o);
+#pragma unroll
+      for (int c = 0; c < N; ++c) A2[t + N2 * c] = o[c];
+#pragma unroll
+      for (int k = 0; k < N; ++k) L[k] = A1[t + N2 * k];
+      gline<P, 2>(L, o);
+#pragma unroll
+      for (int c = 0; c < N; ++c) A1[t + N2 * c] = o[c];
     }
     __syncthreads();
     {  // factors consumed: next group's TMA copy and the L2 prefetch of the group after
       const long long nx = grp + gstride;
       if (nx < ngroups && threadIdx.x == 0) {
-        fence_proxy_async_smem();
-        bulk_load(sG, G + nx * C::EPB * 6 * N3, group_bytes(nx), bar);
-        if (nx + gstride < ngroups) gauss_prefetch_l2(G + (nx + gstride) * C::EPB * 6 * N3, group_bytes(nx + gstride));
+        if (GS) {
+          fence_proxy_async_smem();
+          bulk_load(sG, G + nx * C::EPB * 6 * N3, group_bytes(nx), bar);
+          if (nx + gstride < ngroups) gauss_prefetch_l2(G + (nx + gstride) * C::EPB * 6 * N3, group_bytes(nx + gstride));
+        } else {
+          gauss_prefetch_l2(G + nx * C::EPB * 6 * N3, group_bytes(nx));
+        }
       }
     }
     {  // y^T: line (i = t0, c = t1): T0 = B^T Z0 -> A2 (in place), Tb = DB^T Z1 + B^T Z2 -> A1 (in place)

@@ -39,11 +39,12 @@ def levels(S, orc, d):
     return g, o
 
 
-# 3 <= p <= 8 run k_apply_gauss_v2 (TMA-staged factors, persistent blocks, even-odd line products for even
-# p); the larger meshes give its blocks several groups each, ragged last groups and all three boundary kinds
+# 3 <= p <= 16 run k_apply_gauss_v2 (persistent blocks, even-odd line products for even p, TMA-staged factors
+# for p <= 8); the larger meshes give its blocks several groups each, ragged last groups and all three boundary kinds
 @pytest.mark.parametrize("p,shape", [(1, (2, 3, 2)), (2, (2, 2, 3)), (3, (2, 1, 2)), (4, (2, 2, 1)), (5, (1, 2, 1)),
                                      (8, (1, 1, 2)), (16, (1, 1, 1)), (6, (2, 1, 1)), (7, (1, 2, 1)),
-                                     (4, (11, 7, 9)), (3, (13, 9, 10)), (8, (9, 8, 10))])
+                                     (4, (11, 7, 9)), (3, (13, 9, 10)), (8, (9, 8, 10)), (9, (2, 1, 1)), (12, (1, 2, 1)),
+                                     (11, (1, 1, 2)), (16, (3, 2, 2))])
 def test_gauss_operator_parity(S, gauss_orc, p, shape):
     orc = gauss_orc
     d = inputs.problem(shape[0], p, ney=shape[1], nez=shape[2], **WARP)
