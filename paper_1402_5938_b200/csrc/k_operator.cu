@@ -891,6 +891,7 @@ __global__ void __launch_bounds__(V4Cfg<P, GS>::THREADS, V4Cfg<P, GS>::MINB)
 
 
 #include "k_apply_ks.cuh"
+#include "k_apply_v6.cuh"
 
 template <int P>
 static void build_ks_tables(const std::vector<double>& D, const std::vector<double>& eo6, double* out) {
@@ -1514,6 +1515,31 @@ static bool color_enabled() {
   return on;
 }
 
+// SFMG_V6=1: the two-blocks-per-SM kernel for even p >= 12 (k_apply_v6.cuh; measured in
+// profiles/r02_experiments.md)
+static bool v6_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("SFMG_V6");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+template <int P, bool DIR>
+static cudaError_t launch_v6(const MeshDev& m, const double* G, const double* u, double* v, int wait_mode,
+                             int write_bnd, cudaStream_t s) {
+  using C = V6Cfg<P>;
+  static IntPerDevice occ;
+  int resident = 0;
+  cudaError_t e = persistent_blocks(occ, k_apply_v6<P, DIR>, C::THREADS, C::SMEM, resident);
+  if (e) return e;
+  long long grid = (long long)resident * num_sms();
+  if (grid > m.E) grid = m.E;
+  MeshDev mm = m;
+  mm.pdl_early = early_pdl(m) ? 1 : 0;
+  return launch_pdl(k_apply_v6<P, DIR>, (unsigned)grid, (unsigned)C::THREADS, C::SMEM, s, mm, G, u, v, wait_mode,
+                    write_bnd);
+}
+
 template <int P, bool DIR, bool IPS>
 static cudaError_t launch_ks(const MeshDev& m, const double* G, const double* u, double* v, int wait_mode,
                              int write_bnd, cudaStream_t s) {
@@ -1562,6 +1588,7 @@ static cudaError_t apply_pd(const MeshDev& m, const double* G, const double* u, 
   } else {
     if constexpr (P >= kKsMinP && P % 2 == 0) {   // even orders: the even-odd line products keep the
                                                    // kernel within the register file (odd p spills)
+      if (v6_enabled()) return launch_v6<P, DIR>(m, G, u, v, wait_mode, write_bnd, s);
       if (ks_enabled()) {
         MeshDev mm = m;
         mm.pdl_early = early_pdl(m) ? 1 : 0;

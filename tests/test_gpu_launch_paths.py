@@ -45,11 +45,15 @@ print(json.dumps(out))
 """
 
 
-@pytest.mark.parametrize("maxn,ksplit", [("0", "0"), (str(1 << 24), "0"), ("0", "1"), (str(1 << 24), "1")],
-                         ids=["completion_ordered", "early_triggers", "ksplit_completion_ordered", "ksplit_early"])
+@pytest.mark.parametrize("maxn,ksplit", [("0", "0"), (str(1 << 24), "0"), ("0", "1"), (str(1 << 24), "1"),
+                                         ("0", "v6"), (str(1 << 24), "v6")],
+                         ids=["completion_ordered", "early_triggers", "ksplit_completion_ordered", "ksplit_early",
+                              "v6_completion_ordered", "v6_early"])
 def test_launch_schedules_match_oracle(maxn, ksplit):
-    """ksplit = 1 routes even p >= 12 to the k-split cluster kernel (k_apply_ks.cuh, opt-in)."""
-    env = dict(os.environ, SFMG_EARLY_MAXN=maxn, SFMG_KSPLIT=ksplit)
+    """ksplit = 1 routes even p >= 12 to the k-split cluster kernel (k_apply_ks.cuh, opt-in); "v6" to the
+    two-blocks-per-SM kernel (k_apply_v6.cuh, opt-in)."""
+    env = dict(os.environ, SFMG_EARLY_MAXN=maxn, SFMG_KSPLIT="1" if ksplit == "1" else "0",
+               SFMG_V6="1" if ksplit == "v6" else "0")
     r = subprocess.run([sys.executable, "-c", SCRIPT % {"root": ROOT}], env=env, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
